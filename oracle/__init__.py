@@ -1,0 +1,241 @@
+"""CPU parity oracle for the longest-repeat path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline /
+reference leg may import this package, and only as the checker or the timed
+CPU baseline -- never as the thing measured or shipped.  The product package
+``paper_1501_06663_b200`` never imports it.
+
+Two layers:
+
+* :mod:`oracle.repeatscan_oracle` (C, built by ``oracle/Makefile`` into
+  ``oracle/liboracle.so``): a line-by-line restatement of the reference
+  ``repeatscan`` kernels (``_kernels_numba.py``), its prefix-doubling suffix
+  sort (``suffixes.py:31-53``) and its engine (``engine.py:43-110``).  Pinned
+  against golden vectors produced by the reference itself
+  (``tests/golden/make_golden.py``), see ``tests/test_oracle_golden.py``.
+* :func:`brute_all_positions` -- the reference's brute-force substring oracle
+  (``oracle.py:78-104``) restated in pure Python, for tiny inputs only.
+
+All arrays use the reference layouts: int64, 1-based with a pad slot 0.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "liboracle.so"
+_lib = None
+
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_U8P = ctypes.POINTER(ctypes.c_uint8)
+
+
+def build() -> Path:
+    """Compile the C restatement (gcc + OpenMP) in place."""
+    subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        build()
+    lib = ctypes.CDLL(str(_LIB_PATH))
+    i64, c_int = ctypes.c_int64, ctypes.c_int
+    sig = {
+        "or_suffix_array_0based": (c_int, [_U8P, i64, _I64P]),
+        "or_build_structures": (c_int, [_U8P, i64, _I64P, _I64P, _I64P]),
+        "or_kasai_lcp": (None, [_U8P, _I64P, _I64P, _I64P, i64]),
+        "or_fill_raw_llr": (None, [i64, i64, _I64P, _I64P, _I64P]),
+        "or_fill_flags": (None, [i64, i64, _I64P, _I64P]),
+        "or_scatter_chunk": (None, [i64, i64, _I64P, _I64P, _I64P, _I64P, _I64P]),
+        "or_compact_sequential": (i64, [_I64P, i64, _I64P, _I64P]),
+        "or_parallel_scan": (None, [_I64P, i64, _I64P, c_int]),
+        "or_build_raw_llr_par": (None, [_I64P, _I64P, i64, _I64P, c_int]),
+        "or_build_compact_llr_par": (i64, [_I64P, i64, _I64P, _I64P, c_int]),
+        "or_leftmost_all_par": (
+            None, [i64, c_int, _I64P, _I64P, _I64P, _I64P, i64, _I64P, _I64P, c_int]),
+        "or_all_count_par": (
+            i64, [i64, c_int, _I64P, _I64P, _I64P, _I64P, i64, _I64P, _I64P, c_int]),
+        "or_all_fill_par": (
+            None, [i64, c_int, _I64P, _I64P, _I64P, _I64P, i64, _I64P, _I64P, _I64P, c_int]),
+        "or_max_threads": (c_int, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_I64P)
+
+
+def _u8(a: np.ndarray):
+    return a.ctypes.data_as(_U8P)
+
+
+def max_threads() -> int:
+    return int(_load().or_max_threads())
+
+
+def _workers(workers: int | None) -> int:
+    return int(workers) if workers else (os.cpu_count() or 1)
+
+
+# -- suffixes.py:56-66 --------------------------------------------------------
+def build_suffix_structures(data: np.ndarray):
+    """(sa, rank, lcp) int64 1-based padded, as ``build_suffix_structures``."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    n = int(data.size)
+    sa = np.zeros(n + 1, np.int64)
+    rank = np.zeros(n + 1, np.int64)
+    lcp = np.zeros(n + 2, np.int64)
+    if n:
+        rc = _load().or_build_structures(_u8(data), n, _p(sa), _p(rank), _p(lcp))
+        if rc != 0:
+            raise MemoryError("oracle suffix sort out of memory")
+    return sa, rank, lcp
+
+
+# -- llr.py ------------------------------------------------------------------
+def build_raw_llr(rank: np.ndarray, lcp: np.ndarray, workers: int | None = 1) -> np.ndarray:
+    n = int(rank.size) - 1
+    out = np.zeros(n + 1, np.int64)
+    _load().or_build_raw_llr_par(_p(rank), _p(lcp), n, _p(out), _workers(workers))
+    return out
+
+
+def compute_flags(raw: np.ndarray) -> np.ndarray:
+    n = int(raw.size) - 1
+    out = np.zeros(n + 1, np.int64)
+    if n:
+        _load().or_fill_flags(1, n + 1, _p(raw), _p(out))
+    return out
+
+
+def prefix_sum(flags: np.ndarray, workers: int | None = 1) -> np.ndarray:
+    ps = np.zeros_like(flags)
+    n = int(flags.size) - 1
+    if n > 0:
+        src = np.ascontiguousarray(flags[1:])
+        dst = np.zeros(n, np.int64)
+        _load().or_parallel_scan(_p(src), n, _p(dst), _workers(workers))
+        ps[1:] = dst
+    return ps
+
+
+def compact_sequential(raw: np.ndarray):
+    n = int(raw.size) - 1
+    s = np.empty(max(n, 1), np.int64)
+    l = np.empty(max(n, 1), np.int64)
+    m = int(_load().or_compact_sequential(_p(raw), n, _p(s), _p(l)))
+    return s[:m].copy(), l[:m].copy()
+
+
+def build_compact_llr(raw: np.ndarray, workers: int | None = 1):
+    """(starts, lengths) 0-based arrays of size m via flag/scan/scatter."""
+    n = int(raw.size) - 1
+    s = np.empty(max(n, 1), np.int64)
+    l = np.empty(max(n, 1), np.int64)
+    m = int(_load().or_build_compact_llr_par(_p(raw), n, _p(s), _p(l), _workers(workers)))
+    return s[:m].copy(), l[:m].copy()
+
+
+# -- query.py:171-215 ----------------------------------------------------------
+_PATHS = {"raw": 0, "compact": 1}
+
+
+def _compact_args(c):
+    if c is None:
+        z = np.zeros(1, np.int64)
+        return z, z, z, 0
+    s, l = c
+    s = np.ascontiguousarray(s, dtype=np.int64)
+    l = np.ascontiguousarray(l, dtype=np.int64)
+    e = s + l - 1
+    m = int(s.size)
+    if m == 0:
+        z = np.zeros(1, np.int64)
+        return z, z, z, 0
+    return s, l, e, m
+
+
+def leftmost_all_positions(n: int, path: str, raw: np.ndarray, c=None, workers: int | None = 1):
+    """(starts, lengths), each int64[n+1]; starts[0] = -1."""
+    starts = np.full(n + 1, -1, np.int64)
+    lengths = np.zeros(n + 1, np.int64)
+    cs, cl, ce, m = _compact_args(c)
+    _load().or_leftmost_all_par(n, _PATHS[path], _p(raw), _p(cs), _p(cl), _p(ce), m,
+                                _p(starts), _p(lengths), _workers(workers))
+    return starts, lengths
+
+
+def all_all_positions(n: int, path: str, raw: np.ndarray, c=None, workers: int | None = 1):
+    """(lengths int64[n+1], offsets int64[n+2], flat_starts int64[T])."""
+    lengths = np.zeros(n + 1, np.int64)
+    offsets = np.zeros(n + 2, np.int64)
+    cs, cl, ce, m = _compact_args(c)
+    lib = _load()
+    w = _workers(workers)
+    total = int(lib.or_all_count_par(n, _PATHS[path], _p(raw), _p(cs), _p(cl), _p(ce), m,
+                                     _p(lengths), _p(offsets), w))
+    flat = np.empty(total, np.int64)
+    if total:
+        lib.or_all_fill_par(n, _PATHS[path], _p(raw), _p(cs), _p(cl), _p(ce), m,
+                            _p(lengths), _p(offsets), _p(flat), w)
+    return lengths, offsets, flat
+
+
+def all_positions(data: np.ndarray, mode: str = "leftmost", path: str = "compact",
+                  workers: int | None = 1, structures=None):
+    """query.py:218-239 over raw bytes; returns the tuple of result arrays."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    sa, rank, lcp = structures if structures is not None else build_suffix_structures(data)
+    n = int(sa.size) - 1
+    raw = build_raw_llr(rank, lcp, workers)
+    c = build_compact_llr(raw, workers) if path == "compact" else None
+    if mode == "leftmost":
+        return leftmost_all_positions(n, path, raw, c, workers)
+    return all_all_positions(n, path, raw, c, workers)
+
+
+# -- oracle.py:78-104 brute force (pure Python; tiny inputs only) -------------
+def _longest_repeat_from(s: bytes, i: int) -> int:
+    """oracle.py:27-38: longest repeated substring starting at 1-based i."""
+    for length in range(len(s) - i + 1, 0, -1):
+        sub = s[i - 1: i - 1 + length]
+        if s.find(sub) != s.rfind(sub):
+            return length
+    return 0
+
+
+def brute_all_positions(s: bytes, mode: str = "leftmost"):
+    """Per-position list: (start, length) for leftmost, list of them for all."""
+    n = len(s)
+    reach = [0] * (n + 1)
+    for i in range(1, n + 1):
+        reach[i] = _longest_repeat_from(s, i)
+    out = []
+    for k in range(1, n + 1):
+        best = 0
+        for i in range(1, k + 1):
+            if reach[i] >= k - i + 1 and reach[i] > best:
+                best = reach[i]
+        if best == 0:
+            out.append((-1, 0) if mode == "leftmost" else [])
+            continue
+        hits = [(i, best) for i in range(1, k + 1) if reach[i] >= best and i + best - 1 >= k]
+        out.append(hits[0] if mode == "leftmost" else hits)
+    return out
