@@ -1,0 +1,175 @@
+/*
+ * repeatscan_b200.h -- C-ABI of the B200-native longest-repeat path.
+ *
+ * Drop-in boundary for the reference package `repeatscan`
+ * (/root/reference/pkg/src/repeatscan, cited below as <file>:<line>).  The
+ * reference has no FFI: its data-parallel path goes through the operator API
+ * `_backend.kernels` (11 chunked numba kernels, _kernels_numba.py:15-195)
+ * driven by `engine.parallel_for/parallel_scan` (engine.py:55-110).  Each
+ * entry point below replaces one reference call site; the ctypes binding in
+ * paper_1501_06663_b200/_native.py mirrors the reference Python API on top.
+ *
+ * Conventions (the reference's host layouts, suffixes.py:3-8, query.py:130-168):
+ *   - every host array is int64, 1-based with an unused pad slot 0:
+ *       sa[n+1], rank[n+1], lcp[n+2], raw[n+1], flags[n+1], ps[n+1],
+ *       leftmost starts/lengths[n+1], all lengths[n+1], offsets[n+2];
+ *     compact starts/lengths and flat tie starts are 0-based [m] / [T].
+ *   - plain host pointers and sizes; no device or torch types cross the ABI.
+ *   - every call is synchronous w.r.t. its host outputs and returns a status;
+ *     rs_last_error() explains a non-zero status.
+ *   - mode: 0 = leftmost, 1 = all ties.   path: 0 = raw, 1 = compact.
+ *   - n <= 2^31 - 2 (device indices are 32-bit; tie totals are 64-bit).
+ */
+#ifndef REPEATSCAN_B200_H
+#define REPEATSCAN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (0 = ok) */
+#define RS_OK 0
+#define RS_EINVAL -1 /* bad argument / malformed input -> ValueError  */
+#define RS_ERANGE -2 /* position / size out of range   -> IndexError  */
+#define RS_ENOMEM -3 /* device or host allocation failed -> MemoryError */
+#define RS_ECUDA -4  /* CUDA runtime error              -> RuntimeError */
+#define RS_ENCCL -5  /* NCCL error                      -> RuntimeError */
+#define RS_ESTATE -6 /* call out of order (e.g. fetch before query)   */
+
+#define RS_MODE_LEFTMOST 0
+#define RS_MODE_ALL 1
+#define RS_PATH_RAW 0
+#define RS_PATH_COMPACT 1
+
+/* stage timers (milliseconds, CUDA events on the context stream) */
+#define RS_STAGE_H2D 0
+#define RS_STAGE_SA 1
+#define RS_STAGE_LCP 2
+#define RS_STAGE_RAW_LLR 3
+#define RS_STAGE_COMPACT 4
+#define RS_STAGE_QUERY 5
+#define RS_STAGE_D2H 6
+#define RS_NUM_STAGES 7
+
+typedef struct rs_ctx rs_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+const char *rs_version(void);
+int rs_device_count(int *count);
+/* One context per process and device: a CUDA stream, a device buffer arena
+ * and the device-resident pipeline state.  Replaces the thread pool of
+ * engine.py:71-74 / :92-109 as the "concurrency boundary". */
+int rs_create(int device, rs_ctx **out);
+int rs_destroy(rs_ctx *ctx);
+const char *rs_last_error(const rs_ctx *ctx);
+int rs_synchronize(rs_ctx *ctx);
+/* number of kernels this context launched so far */
+int rs_launch_count(const rs_ctx *ctx, int64_t *count);
+/* last per-stage device times (RS_NUM_STAGES doubles) */
+int rs_stage_times(const rs_ctx *ctx, double *ms);
+/* CUDA-event timing on the context stream (slots 0..63) */
+int rs_record_event(rs_ctx *ctx, int slot);
+int rs_elapsed_ms(rs_ctx *ctx, int slot_a, int slot_b, float *ms);
+/* bytes of device memory currently held by the arena */
+int rs_device_bytes(const rs_ctx *ctx, int64_t *bytes);
+/* release every device buffer of the arena */
+int rs_release(rs_ctx *ctx);
+/* pinned host memory for zero-staging D2H outputs (cudaHostAlloc) */
+int rs_host_alloc(int64_t bytes, void **out);
+int rs_host_free(void *p);
+
+/* ---- array-level operators (host int64 in / host int64 out) -------------
+ * Each replaces one reference function on caller-allocated arrays. */
+
+/* suffixes.py:56-66 build_suffix_structures: sa[n+1], rank[n+1], lcp[n+2]
+ * (zero-filled pads) from text[n]; prefix doubling + LSD radix sort on device,
+ * rank by inversion, Kasai/PLCP LCP. */
+int rs_suffix_structures(rs_ctx *ctx, const uint8_t *text, int64_t n, int64_t *sa,
+                         int64_t *rank, int64_t *lcp);
+/* llr.py:63-72 build_raw_llr -> _kernels_numba.py:33-38 fill_raw_llr */
+int rs_raw_llr(rs_ctx *ctx, const int64_t *rank, const int64_t *lcp, int64_t n, int64_t *raw);
+/* llr.py:84-89 compute_flags -> _kernels_numba.py:41-46 fill_flags */
+int rs_flags(rs_ctx *ctx, const int64_t *raw, int64_t n, int64_t *flags);
+/* llr.py:92-96 prefix_sum -> engine.py:77-110 parallel_scan (inclusive over
+ * slots 1..n of an (n+1)-array; ps[0] = 0) */
+int rs_prefix_sum(rs_ctx *ctx, const int64_t *flags, int64_t n, int64_t *ps);
+/* engine.py:77-110 parallel_scan on a plain 0-based array of `count` values */
+int rs_inclusive_scan(rs_ctx *ctx, const int64_t *values, int64_t count, int64_t *out);
+/* llr.py:99-116 scatter_compact -> _kernels_numba.py:49-55 scatter_chunk;
+ * starts/lengths hold ps[n] entries */
+int rs_scatter_compact(rs_ctx *ctx, const int64_t *raw, const int64_t *flags, const int64_t *ps,
+                       int64_t n, int64_t *starts, int64_t *lengths);
+/* llr.py:119-123 build_compact_llr (fused flag -> scan -> scatter) and
+ * llr.py:75-81 compact_llr_sequential (same result).  starts/lengths must
+ * hold n entries; *m receives the entry count. */
+int rs_compact(rs_ctx *ctx, const int64_t *raw, int64_t n, int64_t *starts, int64_t *lengths,
+               int64_t *m);
+
+/* ---- device-resident pipeline (query.py:218-239 all_positions) ----------
+ * load text or structures once, run the query on device, fetch results. */
+
+/* Text bytes (text.py:21-23 uint8 buffer), H2D. */
+int rs_set_text(rs_ctx *ctx, const uint8_t *text, int64_t n);
+/* query.py:234 `structures=` input (range-checked on device).  sa may be
+ * NULL: the query path only reads rank and lcp (_kernels_numba.py:33-38). */
+int rs_set_structures(rs_ctx *ctx, const int64_t *sa, const int64_t *rank, const int64_t *lcp,
+                      int64_t n);
+/* suffixes.py:69-103 verify_suffix_structures, on device; *ok = 1 iff valid.
+ * (size and sentinel checks are the caller's, as in the reference). */
+int rs_verify_structures(rs_ctx *ctx, const uint8_t *text, int64_t n, const int64_t *sa,
+                         const int64_t *rank, const int64_t *lcp, int64_t *ok);
+/* query.py:234 build_suffix_structures on device from the loaded text. */
+int rs_build_structures(rs_ctx *ctx);
+int rs_get_structures(rs_ctx *ctx, int64_t *sa, int64_t *rank, int64_t *lcp);
+/* query.py:171-215 `raw` / `c` inputs given by the caller. */
+int rs_set_raw(rs_ctx *ctx, const int64_t *raw, int64_t n);
+int rs_set_compact(rs_ctx *ctx, const int64_t *starts, const int64_t *lengths, int64_t m,
+                   int64_t n);
+/* query.py:235-239: raw LLR (if absent) -> compaction (compact path, if
+ * absent) -> per-position scan.  For mode=all, *total receives T, the
+ * number of tie starts (may be NULL). */
+int rs_query(rs_ctx *ctx, int mode, int path, int64_t *total);
+/* Leftmost results: starts[n+1] (starts[0] = -1), lengths[n+1]. */
+int rs_fetch_leftmost(rs_ctx *ctx, int64_t *starts, int64_t *lengths);
+/* All-ties results: lengths[n+1], offsets[n+2], flat[T]. */
+int rs_fetch_all(rs_ctx *ctx, int64_t *lengths, int64_t *offsets, int64_t *flat);
+/* Intermediate arrays of the pipeline (for build_raw_llr / build_compact_llr). */
+int rs_get_raw(rs_ctx *ctx, int64_t *raw);
+int rs_get_compact_size(rs_ctx *ctx, int64_t *m);
+int rs_get_compact(rs_ctx *ctx, int64_t *starts, int64_t *lengths);
+/* Invalidate the pipeline state (keeps the buffer arena). */
+int rs_reset(rs_ctx *ctx);
+/* Number of prefix-doubling rounds of the last on-device suffix sort. */
+int rs_sa_rounds(const rs_ctx *ctx, int *rounds);
+
+/* ---- sharded query (multi-GPU) ------------------------------
+ * One process per GPU.  The compact entries of the WHOLE text live in every
+ * rank's device buffer (rank 0 builds them, torch.distributed/NCCL broadcasts
+ * them straight into the buffer returned by rs_device_buffer).  Each rank
+ * answers its position shard [lo, hi) (1-based); the shard's left halo is
+ * implicit: the per-tile windows are found by binary search over the global
+ * entry array (ends strictly increasing), so entries that start before lo
+ * but still cover it are included.  Shard outputs are shard-local:
+ * leftmost starts/lengths[hi-lo]; all lengths[hi-lo], offsets[hi-lo+1]
+ * (offsets[0] = 0, local), flat[T_shard]. */
+#define RS_BUF_LLRC 0  /* uint32 pairs (start, length), 8 bytes per entry */
+#define RS_BUF_OUT0 1  /* int64 */
+#define RS_BUF_OUT1 2  /* int64 */
+#define RS_BUF_FLAT 3  /* int64 */
+/* Ensure >= bytes of device buffer `which` and return its device pointer. */
+int rs_device_buffer(rs_ctx *ctx, int which, int64_t bytes, void **ptr);
+/* Declare that RS_BUF_LLRC holds m valid entries of a text of length n
+ * (validated on device like rs_set_compact). */
+int rs_set_compact_device(rs_ctx *ctx, int64_t m, int64_t n);
+/* cudaStream_t of the context (for torch.cuda.ExternalStream). */
+int rs_stream(rs_ctx *ctx, void **stream);
+int rs_query_shard(rs_ctx *ctx, int mode, int64_t lo, int64_t hi, int64_t *total);
+/* D2H of the shard results (a, b, flat as described above). */
+int rs_fetch_shard(rs_ctx *ctx, int mode, int64_t *a, int64_t *b, int64_t *flat);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

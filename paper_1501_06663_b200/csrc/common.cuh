@@ -1,0 +1,299 @@
+// common.cuh -- shared runtime pieces of librepeatscan_b200 (sm_100a only).
+//
+// * rs_ctx: one per process per device; owns a stream, a grow-only device
+//   buffer arena, CUDA events and the device-resident pipeline state.
+// * RsError: internal exception; the C-ABI (capi.cu) maps it to a status code
+//   plus rs_last_error().
+// * Decoupled look-back (single-pass scan) primitives used by compaction,
+//   the all-ties scan, the radix sort and the group-head scans.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/repeatscan_b200.h"
+
+namespace rsb {
+
+typedef unsigned long long u64;
+typedef long long i64;
+
+struct RsError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string &msg);
+void check_cuda(cudaError_t e, const char *what, const char *file, int line);
+#define RS_CUDA(x) ::rsb::check_cuda((x), #x, __FILE__, __LINE__)
+
+enum BufId {
+    B_TEXT = 0,
+    B_SA,
+    B_ISA,
+    B_LCP,
+    B_RAW,
+    B_LLRC,      // uint2 (start, len) compact entries
+    B_BOUNDS,    // per-grain (lo, hi) for the scan kernels
+    B_OUT0,      // int64 answers: leftmost starts | all lengths
+    B_OUT1,      // int64 answers: leftmost lengths | all offsets
+    B_FLAT,      // int64 tie starts
+    B_KEYS0,
+    B_KEYS1,
+    B_VALS0,
+    B_VALS1,
+    B_SCRATCH,   // look-back status words + counters
+    B_HIST,      // radix histograms
+    B_PHI,
+    B_PLCP,
+    B_T0,
+    B_T1,
+    B_T2,
+    B_T3,
+    B_I64A,      // staging for int64 API arrays
+    B_I64B,
+    B_I64C,
+    B_I64D,
+    B_SMALL,     // small device scalars (error flags, counts)
+    B_COUNT
+};
+
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+constexpr int kMaxEvents = 64;
+
+}  // namespace rsb
+
+struct rs_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    rsb::Buf bufs[rsb::B_COUNT];
+    long long launches = 0;
+    cudaEvent_t events[rsb::kMaxEvents] = {};
+    void *small_host = nullptr;  // pinned scratch for scalar readbacks
+    // pipeline state
+    long long n = -1;
+    bool have_text = false;
+    bool have_sa = false;   // SA + ISA on device
+    bool have_lcp = false;  // SA-order LCP on device
+    bool have_raw = false;
+    bool have_compact = false;
+    long long m = 0;
+    int out_mode = -1;      // 0 leftmost, 1 all (what B_OUT* hold)
+    long long total = 0;    // tie total of the last all-ties query
+    int sa_rounds = 0;      // prefix-doubling rounds of the last SA build
+    long long shard_lo = 0, shard_hi = 0;
+    double stage_ms[RS_NUM_STAGES] = {};
+};
+
+namespace rsb {
+
+void *buf(rs_ctx *c, BufId id, size_t bytes);
+void fetch_small(rs_ctx *c, void *host, const void *dev, size_t bytes);
+
+// Counts one kernel launch and surfaces launch errors.
+void after_launch(rs_ctx *c, const char *name);
+#define RS_LAUNCH(ctx, kernel, grid, block, smem, ...)                         \
+    do {                                                                       \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);      \
+        ::rsb::after_launch((ctx), #kernel);                                   \
+    } while (0)
+
+inline unsigned grid_for(long long items, int per_block) {
+    long long g = (items + per_block - 1) / per_block;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+// ----------------------------------------------------------------------------
+// Decoupled look-back.  Status word: bits 63..62 = flag (0 invalid,
+// 1 aggregate, 2 inclusive prefix), bits 61..0 = value.
+// ----------------------------------------------------------------------------
+constexpr u64 kFlagAgg = 1ull << 62;
+constexpr u64 kFlagPre = 2ull << 62;
+constexpr u64 kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_relaxed(u64 *p, u64 v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_relaxed(const u64 *p) {
+    u64 v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct OpSum {
+    __device__ __forceinline__ u64 operator()(u64 a, u64 b) const { return a + b; }
+    static constexpr u64 identity = 0;
+};
+struct OpMax {
+    __device__ __forceinline__ u64 operator()(u64 a, u64 b) const { return a > b ? a : b; }
+    static constexpr u64 identity = 0;
+};
+
+template <typename Op>
+__device__ __forceinline__ u64 warp_reduce(u64 v, Op op) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Called by ONE full warp of the tile.  Publishes `aggregate` for `tile`,
+// looks back over predecessors and returns the exclusive prefix (identical
+// in every lane).  status[] must be zeroed before the launch.
+template <typename Op>
+__device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(&status[0], kFlagPre | (aggregate & kValMask));
+        return Op::identity;
+    }
+    if (lane == 0) st_relaxed(&status[tile], kFlagAgg | (aggregate & kValMask));
+    u64 exclusive = Op::identity;
+    long long base = tile - 1;
+    while (true) {
+        long long idx = base - lane;
+        u64 s;
+        if (idx >= 0) {
+            do {
+                s = ld_relaxed(&status[idx]);
+            } while ((s >> 62) == 0);
+        } else {
+            s = kFlagPre | Op::identity;
+        }
+        unsigned pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        int first = pre ? __ffs(pre) - 1 : 32;
+        u64 v = (lane <= first) ? (s & kValMask) : Op::identity;
+        v = warp_reduce(v, op);
+        exclusive = op(exclusive, v);
+        if (pre) break;
+        base -= 32;
+    }
+    if (lane == 0) st_relaxed(&status[tile], kFlagPre | (op(exclusive, aggregate) & kValMask));
+    return exclusive;
+}
+
+// Block-wide exclusive sum of one u32 per thread; returns the block total.
+template <int NT>
+__device__ __forceinline__ unsigned block_exclusive_sum(unsigned v, unsigned &excl,
+                                                        unsigned *s_warp /*[NT/32]*/) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = (lane < NT / 32) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    unsigned warp_base = warp ? s_warp[warp - 1] : 0;
+    excl = warp_base + x - v;
+    unsigned total = s_warp[NT / 32 - 1];
+    __syncthreads();
+    return total;
+}
+
+// 64-bit variant.
+template <int NT>
+__device__ __forceinline__ u64 block_exclusive_sum64(u64 v, u64 &excl, u64 *s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u64 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        u64 w = (lane < NT / 32) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    u64 warp_base = warp ? s_warp[warp - 1] : 0;
+    excl = warp_base + x - v;
+    u64 total = s_warp[NT / 32 - 1];
+    __syncthreads();
+    return total;
+}
+
+// Block-wide inclusive max-scan of one u64 per thread.
+template <int NT>
+__device__ __forceinline__ u64 block_inclusive_max64(u64 v, u64 &incl, u64 *s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u64 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = x > y ? x : y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        u64 w = (lane < NT / 32) ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w = w > y ? w : y;
+        }
+        if (lane < NT / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    u64 wb = warp ? s_warp[warp - 1] : 0;
+    incl = x > wb ? x : wb;
+    u64 total = s_warp[NT / 32 - 1];
+    __syncthreads();
+    return total;
+}
+
+// Scratch layout for single-pass kernels: [counter (u64)] [status words ...].
+struct Scratch {
+    unsigned *counter;
+    u64 *status;
+};
+// Zeroes and returns scratch for `tiles` look-back tiles (async on ctx stream).
+Scratch scratch(rs_ctx *c, long long tiles, int slot = 0);
+
+// ----------------------------------------------------------------------------
+// Host-side stage entry points (defined in the .cu files).
+// ----------------------------------------------------------------------------
+// compact.cu
+long long compact_from_raw(rs_ctx *c, long long n);                 // B_RAW -> B_LLRC, returns m
+void raw_from_rank_lcp(rs_ctx *c, long long n);                     // B_ISA(rank-1), B_LCP -> B_RAW
+void narrow_i64_to_u32(rs_ctx *c, const long long *d_in, unsigned *d_out, long long count,
+                       long long lo, long long hi, long long add, const char *what);
+void widen_u32_to_i64(rs_ctx *c, const unsigned *d_in, long long *d_out, long long count,
+                      long long add);
+// scan_query.cu
+void query(rs_ctx *c, long long n, int mode, int path);  // -> B_OUT0/B_OUT1/B_FLAT
+// suffix_array.cu
+void build_suffix_array(rs_ctx *c, long long n);         // B_TEXT -> B_SA, B_ISA
+void build_lcp(rs_ctx *c, long long n);                  // B_TEXT, B_SA, B_ISA -> B_LCP
+// radix_sort.cu
+// Sorts (keys, vals) pairs by the low `bits` bits of keys, stable.  Result
+// lands in the returned buffers (ping-pong between the two given pairs).
+void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsigned *vals_alt,
+                      long long count, int bits, u64 **keys_out, unsigned **vals_out);
+
+}  // namespace rsb

@@ -1,0 +1,211 @@
+// radix_sort.cu -- hand-written LSD radix sort of (u64 key, u32 value) pairs.
+//
+// Used by the prefix-doubling suffix sort (suffix_array.cu), replacing the
+// reference's np.argsort / np.lexsort (suffixes.py:34, :43).  B200 design:
+//   * one histogram kernel reads the keys ONCE and builds the digit histograms
+//     of every pass (8-bit digits);
+//   * one "onesweep" kernel per pass: tile ranking with warp match_any, a
+//     per-digit decoupled look-back across tiles for the global digit offsets,
+//     and a shared-memory exchange so the scatter writes contiguous runs;
+//   * passes whose digit is constant over all keys are skipped.
+// HBM traffic per pass: read 12 B + write 12 B per pair.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rsb {
+
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kIPT = 16;
+constexpr int kTile = kNT * kIPT;  // 4096 pairs per tile
+constexpr int kWarps = kNT / 32;
+constexpr int kRadix = 256;
+
+__global__ void __launch_bounds__(kNT) k_histograms(const u64 *__restrict__ keys, long long count, int passes,
+                                                    unsigned long long *__restrict__ hist /*[passes][256]*/) {
+    __shared__ unsigned s_hist[8][kRadix];
+    for (int i = threadIdx.x; i < 8 * kRadix; i += kNT) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    long long stride = (long long)gridDim.x * kNT;
+    for (long long i = blockIdx.x * (long long)kNT + threadIdx.x; i < count; i += stride) {
+        u64 k = keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += kNT) {
+        unsigned v = (&s_hist[0][0])[i];
+        if (v) atomicAdd(&hist[i], (unsigned long long)v);
+    }
+}
+
+// Exclusive scan of each pass's 256 counts, in place (one block per pass).
+__global__ void k_hist_scan(unsigned long long *hist) {
+    __shared__ unsigned long long s[kRadix];
+    unsigned long long *h = hist + blockIdx.x * kRadix;
+    s[threadIdx.x] = h[threadIdx.x];
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+        unsigned long long v = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+        __syncthreads();
+        s[threadIdx.x] += v;
+        __syncthreads();
+    }
+    h[threadIdx.x] = s[threadIdx.x] - h[threadIdx.x];
+}
+
+struct SortSmem {
+    u64 keys[kTile];
+    unsigned vals[kTile];
+    unsigned short warp_cnt[kWarps][kRadix];  // per-warp digit counts, then warp offsets
+    unsigned tile_start[kRadix];              // exclusive scan of tile digit counts
+    unsigned long long global_base[kRadix];
+    unsigned tile_id;
+};
+
+__global__ void __launch_bounds__(kNT) k_onesweep(const u64 *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
+                                                  u64 *__restrict__ keys_out, unsigned *__restrict__ vals_out,
+                                                  long long count, int shift,
+                                                  const unsigned long long *__restrict__ digit_base,
+                                                  unsigned *counter, u64 *status /*[tiles][256]*/) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kWarps * kRadix; i += kNT) (&sm.warp_cnt[0][0])[i] = 0;
+    if (threadIdx.x == 0) sm.tile_id = atomicAdd(counter, 1u);
+    __syncthreads();
+    const long long tile = sm.tile_id;
+    const long long base = tile * kTile + (long long)warp * (kIPT * 32);
+
+    u64 k[kIPT];
+    unsigned v[kIPT];
+    unsigned short rank[kIPT];
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        long long idx = base + i * 32 + lane;
+        if (idx < count) {
+            k[i] = keys_in[idx];
+            v[i] = vals_in[idx];
+        }
+    }
+    const unsigned lt_mask = (1u << lane) - 1;
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        long long idx = base + i * 32 + lane;
+        bool valid = idx < count;
+        unsigned d = valid ? (unsigned)(k[i] >> shift) & 0xff : 0x100u;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned short before = valid ? sm.warp_cnt[warp][d & 0xff] : 0;
+        __syncwarp();
+        if (valid) {
+            rank[i] = before + (unsigned short)__popc(peers & lt_mask);
+            if ((peers & lt_mask) == 0) sm.warp_cnt[warp][d] = before + (unsigned short)__popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: warp exclusive offsets + tile total; publish + look back
+    {
+        const int d = threadIdx.x;  // kNT == kRadix
+        unsigned run = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            unsigned c = sm.warp_cnt[w][d];
+            sm.warp_cnt[w][d] = (unsigned short)run;
+            run += c;
+        }
+        // tile-local digit start: block exclusive scan over digits
+        unsigned excl;
+        __shared__ unsigned s_w[kNT / 32];
+        block_exclusive_sum<kNT>(run, excl, s_w);
+        sm.tile_start[d] = excl;
+        // decoupled look-back for this digit across tiles
+        u64 *st = status + (size_t)tile * kRadix + d;
+        u64 prefix = 0;
+        if (tile == 0) {
+            st_relaxed(st, kFlagPre | run);
+        } else {
+            st_relaxed(st, kFlagAgg | run);
+            long long t = tile - 1;
+            while (true) {
+                u64 s;
+                do {
+                    s = ld_relaxed(status + (size_t)t * kRadix + d);
+                } while ((s >> 62) == 0);
+                prefix += s & kValMask;
+                if ((s >> 62) == 2) break;
+                --t;
+            }
+            st_relaxed(st, kFlagPre | (prefix + run));
+        }
+        sm.global_base[d] = digit_base[d] + prefix;
+    }
+    __syncthreads();
+    // exchange through shared memory into digit order
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        long long idx = base + i * 32 + lane;
+        if (idx < count) {
+            unsigned d = (unsigned)(k[i] >> shift) & 0xff;
+            unsigned pos = sm.tile_start[d] + sm.warp_cnt[warp][d] + rank[i];
+            sm.keys[pos] = k[i];
+            sm.vals[pos] = v[i];
+        }
+    }
+    __syncthreads();
+    long long tile_count = count - tile * kTile;
+    if (tile_count > kTile) tile_count = kTile;
+    for (int j = threadIdx.x; j < tile_count; j += kNT) {
+        u64 key = sm.keys[j];
+        unsigned d = (unsigned)(key >> shift) & 0xff;
+        unsigned long long dst = sm.global_base[d] + (j - sm.tile_start[d]);
+        keys_out[dst] = key;
+        vals_out[dst] = sm.vals[j];
+    }
+}
+
+}  // namespace
+
+void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsigned *vals_alt,
+                      long long count, int bits, u64 **keys_out, unsigned **vals_out) {
+    *keys_out = keys;
+    *vals_out = vals;
+    if (count <= 1 || bits <= 0) return;
+    int passes = (bits + 7) / 8;
+    if (passes > 8) passes = 8;
+    unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * kRadix);
+    RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
+    unsigned hist_blocks = (unsigned)std::min<long long>((count + kNT * 16 - 1) / (kNT * 16), c->sm_count * 8);
+    RS_LAUNCH(c, k_histograms, hist_blocks, kNT, 0, keys, count, passes, hist);
+    // Host needs the histograms to skip constant-digit passes.
+    std::vector<unsigned long long> h((size_t)passes * kRadix);
+    fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
+    RS_LAUNCH(c, k_hist_scan, passes, kRadix, 0, hist);
+
+    static bool attr_set = false;
+    if (!attr_set) {
+        RS_CUDA(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(SortSmem)));
+        attr_set = true;
+    }
+    long long tiles = (count + kTile - 1) / kTile;
+    u64 *kin = keys, *kout = keys_alt;
+    unsigned *vin = vals, *vout = vals_alt;
+    for (int p = 0; p < passes; ++p) {
+        bool trivial = false;
+        for (int d = 0; d < kRadix; ++d)
+            if (h[(size_t)p * kRadix + d] == (unsigned long long)count) trivial = true;
+        if (trivial) continue;
+        Scratch s = scratch(c, tiles * kRadix);
+        RS_LAUNCH(c, k_onesweep, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout, vout, count, 8 * p,
+                  hist + (size_t)p * kRadix, s.counter, s.status);
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    *keys_out = kin;
+    *vals_out = vin;
+}
+
+}  // namespace rsb

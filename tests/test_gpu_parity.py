@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path through the C-ABI vs the reference (golden) and the oracle.
+
+Bit-exact for every array (integer work).  Golden vectors come from the
+reference package itself (tests/golden/make_golden.py); larger inputs are
+checked against the pinned C oracle or reference digests.
+"""
+
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1501_06663_b200 as rb
+from paper_1501_06663_b200 import workloads
+from conftest import digest, golden_cases, golden_digests
+
+pytestmark = pytest.mark.gpu
+
+
+def _structs(c):
+    return rb.SuffixStructures(sa=c.sa, rank=c.rank, lcp=c.lcp)
+
+
+def test_suffix_structures_golden():
+    for c in golden_cases():
+        s = rb.build_suffix_structures(rb.Text(c.data))
+        assert np.array_equal(s.sa, c.sa), c
+        assert np.array_equal(s.rank, c.rank), c
+        assert np.array_equal(s.lcp, c.lcp), c
+
+
+def test_llr_pipeline_golden():
+    for c in golden_cases():
+        raw = rb.build_raw_llr(_structs(c))
+        assert np.array_equal(raw, c.raw), c
+        flags = rb.compute_flags(c.raw)
+        assert np.array_equal(flags, c.flags), c
+        ps = rb.prefix_sum(c.flags)
+        assert np.array_equal(ps, c.ps), c
+        sc = rb.scatter_compact(c.raw, c.flags, c.ps)
+        assert np.array_equal(sc.starts, c.c_starts) and np.array_equal(sc.lengths, c.c_lengths), c
+        cc = rb.build_compact_llr(c.raw, rb.ExecPolicy.parallel(3))
+        assert np.array_equal(cc.starts, c.c_starts) and np.array_equal(cc.lengths, c.c_lengths), c
+        cs = rb.compact_llr_sequential(c.raw)
+        assert cs.entries() == cc.entries()
+
+
+def test_all_positions_golden_every_path():
+    for c in golden_cases():
+        t = rb.Text(c.data)
+        for path in ("raw", "compact"):
+            for structures in (None, _structs(c)):
+                L = rb.all_positions(t, mode="leftmost", path=path, structures=structures)
+                assert np.array_equal(L.starts, c.l_starts), (c, path)
+                assert np.array_equal(L.lengths, c.l_lengths), (c, path)
+                A = rb.all_positions(t, mode="all", path=path, structures=structures)
+                assert np.array_equal(A.lengths, c.a_lengths), (c, path)
+                assert np.array_equal(A.offsets, c.a_offsets), (c, path)
+                assert np.array_equal(A.flat_starts, c.a_flat), (c, path)
+
+
+def test_private_batch_drivers_golden():
+    # query.py:171-215 called directly, as cli.py:229-232 and the acceptance tests do
+    from paper_1501_06663_b200.query import _all_all_positions, _leftmost_all_positions
+    for c in golden_cases()[::3]:
+        comp = rb.CompactLlr.from_arrays(c.c_starts, c.c_lengths)
+        for path in ("raw", "compact"):
+            L = _leftmost_all_positions(c.n, path, c.raw, comp, None)
+            assert np.array_equal(L.starts, c.l_starts) and np.array_equal(L.lengths, c.l_lengths)
+            A = _all_all_positions(c.n, path, c.raw, comp, rb.ExecPolicy.parallel(2))
+            assert np.array_equal(A.offsets, c.a_offsets) and np.array_equal(A.flat_starts, c.a_flat)
+
+
+def test_reference_known_answers():
+    t = rb.Text.from_str("mississippi")
+    s = rb.build_suffix_structures(t)
+    assert s.sa[1:].tolist() == [11, 8, 5, 2, 1, 10, 9, 7, 4, 6, 3]
+    assert s.lcp[1:].tolist() == [0, 1, 1, 4, 0, 0, 1, 0, 2, 1, 3, 0]
+    assert rb.verify_suffix_structures(t, s)
+    res = rb.all_positions(t)
+    got = [tuple(res.answer(k)) for k in range(1, 12)]
+    assert got == [(-1, 0), (2, 4), (2, 4), (2, 4), (2, 4), (5, 4), (5, 4), (5, 4), (9, 1),
+                   (10, 1), (11, 1)]
+    for path in ("raw", "compact"):
+        r = rb.all_positions(rb.Text.from_str("abcabcddbca"), mode="all", path=path)
+        assert r.answers(2) == [rb.LrAnswer(1, 3), rb.LrAnswer(2, 3)]
+    e = rb.all_positions(rb.Text.from_str(""))
+    assert e.n == 0 and e.starts.tolist() == [-1]
+    e = rb.all_positions(rb.Text.from_str(""), mode="all")
+    assert e.offsets.tolist() == [0, 0]
+    a4 = rb.all_positions(rb.Text.from_str("aaaa"), mode="all")
+    assert a4.offsets.tolist() == [0, 0, 1, 3, 5, 6] and a4.flat_starts.tolist() == [1, 1, 2, 1, 2, 2]
+
+
+def test_verify_rejects_bad_structures():
+    t = rb.Text.from_str("ab")
+    s = rb.build_suffix_structures(t)
+    bad = rb.SuffixStructures(sa=s.sa[[0, 2, 1]], rank=s.rank.copy(), lcp=s.lcp.copy())
+    assert not rb.verify_suffix_structures(t, bad)
+    t = rb.Text.from_str("aaaa")
+    s = rb.build_suffix_structures(t)
+    lcp = s.lcp.copy()
+    lcp[3] += 1
+    assert not rb.verify_suffix_structures(t, rb.SuffixStructures(sa=s.sa, rank=s.rank, lcp=lcp))
+
+
+def test_exhaustive_binary_strings_vs_oracle():
+    # test_acceptance.py:114-119 shape: every {a,b} string up to n = 12
+    for n in range(1, 13):
+        for tup in itertools.product(b"ab", repeat=n):
+            data = np.frombuffer(bytes(tup), np.uint8)
+            t = rb.Text(data)
+            wl, wo, wf = oracle.all_positions(data, mode="all")
+            A = rb.all_positions(t, mode="all", path="compact")
+            assert np.array_equal(A.offsets, wo) and np.array_equal(A.flat_starts, wf), bytes(tup)
+            if n <= 8:
+                B = rb.all_positions(t, mode="all", path="raw")
+                assert np.array_equal(B.flat_starts, wf)
+
+
+@pytest.mark.parametrize("name", ["acgt_1e6_seed99", "C1_2p20", "C2_shape_2p21", "C4_shape_2p21",
+                                  "C5_shape_2p20", "periodic_2p20"])
+def test_reference_digests(name):
+    rec = golden_digests()[name]
+    data = eval(rec["expr"])
+    t = rb.Text(data)
+    s = rb.build_suffix_structures(t)
+    assert digest(s.sa) == rec["sa"] and digest(s.rank) == rec["rank"] and digest(s.lcp) == rec["lcp"]
+    raw = rb.build_raw_llr(s)
+    assert digest(raw) == rec["raw"]
+    c = rb.build_compact_llr(raw)
+    assert digest(c.starts) == rec["c_starts"] and digest(c.lengths) == rec["c_lengths"]
+    paths = ("raw", "compact") if rec["max_llr"] < 1000 else ("compact",)
+    for path in paths:
+        A = rb.all_positions(t, mode="all", path=path)
+        assert digest(A.lengths) == rec["a_lengths"] and digest(A.offsets) == rec["a_offsets"]
+        assert digest(A.flat_starts) == rec["a_flat"]
+        L = rb.all_positions(t, mode="leftmost", path=path, structures=s)
+        assert digest(L.starts) == rec["l_starts"] and digest(L.lengths) == rec["l_lengths"]
+
+
+def test_random_inputs_vs_oracle(rng):
+    for _ in range(60):
+        n = int(rng.integers(1, 5000))
+        sigma = int(rng.integers(1, 256))
+        alpha = rng.choice(256, size=sigma, replace=False).astype(np.uint8)
+        data = rng.choice(alpha, size=n)
+        if rng.random() < 0.3:  # inject long repeats
+            p = int(rng.integers(1, 50))
+            data = np.resize(data[:p], n)
+        want = oracle.build_suffix_structures(data)
+        s = rb.build_suffix_structures(rb.Text(data))
+        assert all(np.array_equal(a, b) for a, b in zip((s.sa, s.rank, s.lcp), want))
+        wl, wo, wf = oracle.all_positions(data, mode="all", structures=want)
+        A = rb.all_positions(rb.Text(data), mode="all")
+        assert np.array_equal(A.lengths, wl) and np.array_equal(A.offsets, wo)
+        assert np.array_equal(A.flat_starts, wf)
+
+
+def test_tile_boundaries_and_long_windows():
+    # sizes straddling the 2048-position tiles and 4096-key sort tiles,
+    # plus a periodic text whose windows exceed the shared-memory stage.
+    for n in (2047, 2048, 2049, 4095, 4096, 4097, 8191, 8193, 65537):
+        data = workloads.iid_dna(n, n)
+        want = oracle.all_positions(data, mode="all", path="compact")
+        A = rb.all_positions(rb.Text(data), mode="all", path="compact")
+        assert np.array_equal(A.offsets, want[1]) and np.array_equal(A.flat_starts, want[2]), n
+    data = workloads.periodic_mutated(40000, 3, period=7, rate=0.0)
+    for path in ("raw", "compact"):
+        for mode in ("leftmost", "all"):
+            want = oracle.all_positions(data, mode=mode, path="compact")
+            got = rb.all_positions(rb.Text(data), mode=mode, path=path)
+            arrs = (got.starts, got.lengths) if mode == "leftmost" else (
+                got.lengths, got.offsets, got.flat_starts)
+            assert all(np.array_equal(a, b) for a, b in zip(arrs, want)), (path, mode)
+
+
+def test_api_errors():
+    with pytest.raises(ValueError):
+        rb.all_positions(rb.Text.from_str("abc"), mode="bogus")
+    with pytest.raises(ValueError):
+        rb.all_positions(rb.Text.from_str("abc"), path="bogus")
+    with pytest.raises(ValueError):  # raw array violating raw[i] <= raw[i+1] + 1
+        from paper_1501_06663_b200.query import _leftmost_all_positions
+        _leftmost_all_positions(3, "raw", np.array([0, 3, 0, 0], np.int64), None, None)
+    with pytest.raises(ValueError):  # rank out of range
+        rb.build_raw_llr(rb.SuffixStructures(sa=np.array([0, 1], np.int64),
+                                             rank=np.array([0, 5], np.int64),
+                                             lcp=np.zeros(3, np.int64)))
+
+
+def test_parallel_scan_gpu(rng):
+    for _ in range(20):
+        n = int(rng.integers(0, 100000))
+        v = rng.integers(0, 1000, size=n).astype(np.int64)
+        assert np.array_equal(rb.parallel_scan(v, rb.ExecPolicy.parallel(4)), np.cumsum(v))
+
+
+def test_kernels_launch_from_native_library():
+    from paper_1501_06663_b200 import _native
+    ctx = _native.context()
+    before = ctx.launches()
+    rb.all_positions(rb.Text(workloads.iid_dna(10000, 1)), mode="all")
+    assert ctx.launches() > before
