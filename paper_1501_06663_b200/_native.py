@@ -75,7 +75,7 @@ SIGNATURES = {
 _RESTYPES = {"rs_version": ctypes.c_char_p, "rs_last_error": ctypes.c_char_p}
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 def load_library() -> ctypes.CDLL:

@@ -34,7 +34,7 @@ namespace {
 constexpr unsigned kNone = 0xffffffffu;
 
 struct CodeTable {
-    unsigned char code[256];
+    unsigned short code[256];  // 1..sigma; sigma may be 256, so 9 bits
 };
 
 __global__ void k_byte_hist(const unsigned char *__restrict__ text, long long n,
@@ -53,7 +53,7 @@ __global__ void k_byte_hist(const unsigned char *__restrict__ text, long long n,
 __global__ void __launch_bounds__(256) k_init_keys(const unsigned char *__restrict__ text, long long n, CodeTable ct,
                                                    int b, int K, u64 *__restrict__ keys,
                                                    unsigned *__restrict__ vals) {
-    __shared__ unsigned char s[256 + 64];
+    __shared__ unsigned short s[256 + 64];
     long long base = blockIdx.x * 256ll;
     for (int j = threadIdx.x; j < 256 + K; j += 256) {
         long long p = base + j;
@@ -249,7 +249,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * 256);
     CodeTable ct;
     int sigma = 0;
-    for (int b = 0; b < 256; ++b) ct.code[b] = h[b] ? (unsigned char)(++sigma) : 0;
+    for (int b = 0; b < 256; ++b) ct.code[b] = h[b] ? (unsigned short)(++sigma) : 0;
     int bits = 1;
     while ((1 << bits) < sigma + 1) ++bits;
     int K = 64 / bits;
