@@ -141,6 +141,15 @@ int rs_get_compact_size(rs_ctx *ctx, int64_t *m);
 int rs_get_compact(rs_ctx *ctx, int64_t *starts, int64_t *lengths);
 /* Invalidate the pipeline state (keeps the buffer arena). */
 int rs_reset(rs_ctx *ctx);
+/* Drop everything derived from the loaded text (keeps the text resident). */
+int rs_clear_derived(rs_ctx *ctx);
+/* Per-kernel profiling: while enabled every launch is bracketed by CUDA
+ * events on the context stream and tagged with its algorithmic HBM bytes.
+ * rs_profile_end aggregates per kernel name; read them with rs_profile_kernel. */
+int rs_profile_begin(rs_ctx *ctx);
+int rs_profile_end(rs_ctx *ctx, int *kinds);
+int rs_profile_kernel(rs_ctx *ctx, int i, char *name, int cap, int64_t *launches,
+                      double *total_ms, double *bytes);
 /* Number of prefix-doubling rounds of the last on-device suffix sort. */
 int rs_sa_rounds(const rs_ctx *ctx, int *rounds);
 

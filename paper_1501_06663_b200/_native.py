@@ -65,6 +65,11 @@ SIGNATURES = {
     "rs_get_compact_size": [_CTX, _I64P],
     "rs_get_compact": [_CTX, _I64P, _I64P],
     "rs_reset": [_CTX],
+    "rs_clear_derived": [_CTX],
+    "rs_profile_begin": [_CTX],
+    "rs_profile_end": [_CTX, ctypes.POINTER(ctypes.c_int)],
+    "rs_profile_kernel": [_CTX, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, _I64P,
+                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
     "rs_sa_rounds": [_CTX, ctypes.POINTER(ctypes.c_int)],
     "rs_device_buffer": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(_VP)],
     "rs_set_compact_device": [_CTX, ctypes.c_int64, ctypes.c_int64],
@@ -191,6 +196,26 @@ class Context:
         v = _VP()
         self.call("rs_device_buffer", int(which), int(nbytes), ctypes.byref(v))
         return int(v.value)
+
+    def profile_begin(self):
+        self.call("rs_profile_begin")
+
+    def profile_end(self) -> list[dict]:
+        """Per-kernel totals since profile_begin: name, launches, ms, algorithmic bytes."""
+        k = ctypes.c_int()
+        self.call("rs_profile_end", ctypes.byref(k))
+        out = []
+        name = ctypes.create_string_buffer(256)
+        for i in range(k.value):
+            launches = ctypes.c_int64()
+            ms = ctypes.c_double()
+            nbytes = ctypes.c_double()
+            self.call("rs_profile_kernel", i, name, 256, ctypes.byref(launches), ctypes.byref(ms),
+                      ctypes.byref(nbytes))
+            nm = name.value.decode().strip("()")
+            out.append({"kernel": nm, "launches": int(launches.value), "ms": float(ms.value),
+                        "bytes": float(nbytes.value)})
+        return out
 
     def close(self):
         if self.handle:

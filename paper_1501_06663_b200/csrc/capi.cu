@@ -3,9 +3,11 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <algorithm>
 #include <new>
 
 #include "common.cuh"
+#include "scatter.cuh"
 
 namespace rsb {
 
@@ -65,7 +67,25 @@ void fetch_small(rs_ctx *c, void *host, const void *dev, size_t bytes) {
     memcpy(host, c->small_host, bytes);
 }
 
-void after_launch(rs_ctx *c, const char *name) {
+static int prof_event(rs_ctx *c) {
+    int idx = 0;
+    for (const auto &r : c->prof) idx = std::max(idx, r.ev1 + 1);
+    while ((int)c->prof_events.size() <= idx) {
+        cudaEvent_t e;
+        RS_CUDA(cudaEventCreate(&e));
+        c->prof_events.push_back(e);
+    }
+    return idx;
+}
+
+void before_launch(rs_ctx *c) {
+    if (!c->profiling) return;
+    int e0 = prof_event(c);
+    RS_CUDA(cudaEventRecord(c->prof_events[e0], c->stream));
+    c->prof.push_back({nullptr, e0, e0 + 1, 0.0});
+}
+
+void after_launch(rs_ctx *c, const char *name, double bytes) {
     ++c->launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -73,6 +93,21 @@ void after_launch(rs_ctx *c, const char *name) {
         snprintf(b, sizeof(b), "launch of %s failed: %s", name, cudaGetErrorString(e));
         fail(RS_ECUDA, b);
     }
+    if (c->profiling && !c->prof.empty() && c->prof.back().name == nullptr) {
+        auto &r = c->prof.back();
+        while ((int)c->prof_events.size() <= r.ev1) {
+            cudaEvent_t ev;
+            RS_CUDA(cudaEventCreate(&ev));
+            c->prof_events.push_back(ev);
+        }
+        RS_CUDA(cudaEventRecord(c->prof_events[r.ev1], c->stream));
+        r.name = name;
+        r.bytes = bytes;
+    }
+}
+
+void add_bytes_last(rs_ctx *c, double bytes) {
+    if (c->profiling && !c->prof.empty()) c->prof.back().bytes += bytes;
 }
 
 Scratch scratch(rs_ctx *c, long long tiles, int slot) {
@@ -149,6 +184,8 @@ void d2h(rs_ctx *c, void *dst, const void *src, size_t bytes) {
 
 void invalidate(rs_ctx *c) {
     c->have_text = c->have_sa = c->have_lcp = c->have_raw = c->have_compact = false;
+    c->sa_device_built = false;
+    c->raw_from_round0 = false;
     c->out_mode = -1;
     c->n = -1;
 }
@@ -156,6 +193,10 @@ void invalidate(rs_ctx *c) {
 // Ensure the raw LLR array for the pipeline exists (B_RAW, u32, 1-based).
 void ensure_raw(rs_ctx *c, bool *used) {
     if (c->have_raw) return;
+    if (c->have_lcp && c->raw_from_round0) {  // produced during the SA/LCP build
+        c->have_raw = true;
+        return;
+    }
     long long n = c->n;
     if (!c->have_lcp) {
         if (!c->have_sa) {
@@ -170,10 +211,17 @@ void ensure_raw(rs_ctx *c, bool *used) {
         used[RS_STAGE_LCP] = true;
         build_lcp(c, n);
         c->have_lcp = true;
+        if (c->raw_from_round0) {  // the SA/LCP build already produced raw
+            c->have_raw = true;
+            return;
+        }
     }
     Stage st(c, RS_STAGE_RAW_LLR);
     used[RS_STAGE_RAW_LLR] = true;
-    raw_from_rank_lcp(c, n);
+    if (c->have_sa && c->sa_device_built)
+        raw_from_sa_lcp(c, n, raw_slots(n));  // SA order + bucketed scatter (consistent structures)
+    else
+        raw_from_rank_lcp(c, n);  // reference formula on caller-given rank/lcp
     c->have_raw = true;
 }
 
@@ -238,6 +286,7 @@ int rs_destroy(rs_ctx *c) {
         if (c->bufs[i].p) cudaFree(c->bufs[i].p);
     for (int i = 0; i < kMaxEvents; ++i)
         if (c->events[i]) cudaEventDestroy(c->events[i]);
+    for (auto e : c->prof_events) cudaEventDestroy(e);
     if (c->small_host) cudaFreeHost(c->small_host);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -647,6 +696,61 @@ int rs_get_compact(rs_ctx *c, int64_t *starts, int64_t *lengths) {
 
 int rs_reset(rs_ctx *c) {
     return guarded(c, [&] { invalidate(c); });
+}
+
+int rs_clear_derived(rs_ctx *c) {
+    return guarded(c, [&] {
+        if (!c->have_text) fail(RS_ESTATE, "no text loaded");
+        c->have_sa = c->have_lcp = c->have_raw = c->have_compact = false;
+        c->out_mode = -1;
+    });
+}
+
+int rs_profile_begin(rs_ctx *c) {
+    return guarded(c, [&] {
+        c->prof.clear();
+        c->prof_agg.clear();
+        c->profiling = true;
+    });
+}
+
+int rs_profile_end(rs_ctx *c, int *kinds) {
+    return guarded(c, [&] {
+        c->profiling = false;
+        RS_CUDA(cudaStreamSynchronize(c->stream));
+        c->prof_agg.clear();
+        for (const auto &r : c->prof) {
+            if (!r.name) continue;
+            float ms = 0;
+            RS_CUDA(cudaEventElapsedTime(&ms, c->prof_events[r.ev0], c->prof_events[r.ev1]));
+            std::string nm(r.name);
+            auto it = std::find_if(c->prof_agg.begin(), c->prof_agg.end(),
+                                   [&](const rs_ctx::ProfAgg &a) { return a.name == nm; });
+            if (it == c->prof_agg.end()) {
+                c->prof_agg.push_back({nm, 0, 0.0, 0.0});
+                it = c->prof_agg.end() - 1;
+            }
+            it->launches += 1;
+            it->ms += ms;
+            it->bytes += r.bytes;
+        }
+        c->prof.clear();
+        if (kinds) *kinds = (int)c->prof_agg.size();
+    });
+}
+
+int rs_profile_kernel(rs_ctx *c, int i, char *name, int cap, int64_t *launches, double *total_ms,
+                      double *bytes) {
+    return guarded(c, [&] {
+        if (i < 0 || i >= (int)c->prof_agg.size()) fail(RS_ERANGE, "no such profiled kernel");
+        const auto &a = c->prof_agg[i];
+        if (name && cap > 0) {
+            snprintf(name, (size_t)cap, "%s", a.name.c_str());
+        }
+        if (launches) *launches = a.launches;
+        if (total_ms) *total_ms = a.ms;
+        if (bytes) *bytes = a.bytes;
+    });
 }
 
 int rs_sa_rounds(const rs_ctx *c, int *rounds) {

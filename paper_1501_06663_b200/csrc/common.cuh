@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/repeatscan_b200.h"
 
@@ -57,6 +58,10 @@ enum BufId {
     B_I64C,
     B_I64D,
     B_SMALL,     // small device scalars (error flags, counts)
+    B_CURSOR,    // bucketed-scatter fill counts
+    B_T4,
+    B_T5,
+    B_PATCH,     // list of patched LCP slots
     B_COUNT
 };
 
@@ -90,6 +95,27 @@ struct rs_ctx {
     long long total = 0;    // tie total of the last all-ties query
     int sa_rounds = 0;      // prefix-doubling rounds of the last SA build
     long long shard_lo = 0, shard_hi = 0;
+    int sa_key_symbols = 0;                 // K of the round-0 keys
+    long long sa_unsorted_after_round0 = 0; // suffixes left in tied groups by round 0
+    long long sa_final_depth = 0;          // sorted depth when prefix doubling stopped
+    bool lcp_from_keys = false;
+    bool sa_device_built = false;
+    bool raw_from_round0 = false;           // B_RAW filled during the SA build (+ LCP patch fix-up)           // SA/ISA/LCP built here (mutually consistent)             // B_LCP holds round-0 key LCPs (+ unknown marks)
+    // per-kernel profiling (CUDA events around every launch while enabled)
+    bool profiling = false;
+    struct ProfRec {
+        const char *name;
+        int ev0, ev1;
+        double bytes;
+    };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> prof_events;
+    struct ProfAgg {
+        std::string name;
+        long long launches;
+        double ms, bytes;
+    };
+    std::vector<ProfAgg> prof_agg;
     double stage_ms[RS_NUM_STAGES] = {};
 };
 
@@ -98,13 +124,22 @@ namespace rsb {
 void *buf(rs_ctx *c, BufId id, size_t bytes);
 void fetch_small(rs_ctx *c, void *host, const void *dev, size_t bytes);
 
-// Counts one kernel launch and surfaces launch errors.
-void after_launch(rs_ctx *c, const char *name);
-#define RS_LAUNCH(ctx, kernel, grid, block, smem, ...)                         \
+// Counts one kernel launch, surfaces launch errors and, while profiling,
+// brackets it with CUDA events.  `bytes` = algorithmic HBM bytes of the launch
+// (the roofline numerator), 0 if not meaningful.
+void before_launch(rs_ctx *c);
+void after_launch(rs_ctx *c, const char *name, double bytes);
+// Adds algorithmic bytes to the most recent launch (for outputs whose size is
+// only known after the kernel ran, e.g. the tie total).
+void add_bytes_last(rs_ctx *c, double bytes);
+#define RS_LAUNCH_B(ctx, bytes, kernel, grid, block, smem, ...)                \
     do {                                                                       \
+        ::rsb::before_launch(ctx);                                             \
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);      \
-        ::rsb::after_launch((ctx), #kernel);                                   \
+        ::rsb::after_launch((ctx), #kernel, (double)(bytes));                  \
     } while (0)
+#define RS_LAUNCH(ctx, kernel, grid, block, smem, ...) \
+    RS_LAUNCH_B(ctx, 0, kernel, grid, block, smem, __VA_ARGS__)
 
 inline unsigned grid_for(long long items, int per_block) {
     long long g = (items + per_block - 1) / per_block;
@@ -136,6 +171,16 @@ struct OpMax {
     __device__ __forceinline__ u64 operator()(u64 a, u64 b) const { return a > b ? a : b; }
     static constexpr u64 identity = 0;
 };
+// Two scans in one look-back: max over bits 61..31, sum over bits 30..0
+// (both operands < 2^31, sums of n <= 2^31 - 2 items of 0/1 never carry).
+struct OpMaxSum {
+    __device__ __forceinline__ u64 operator()(u64 a, u64 b) const {
+        const u64 m = (1ull << 31) - 1;
+        u64 ha = a >> 31, hb = b >> 31;
+        return ((ha > hb ? ha : hb) << 31) | (((a & m) + (b & m)) & m);
+    }
+    static constexpr u64 identity = 0;
+};
 
 template <typename Op>
 __device__ __forceinline__ u64 warp_reduce(u64 v, Op op) {
@@ -161,9 +206,11 @@ __device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op) 
         long long idx = base - lane;
         u64 s;
         if (idx >= 0) {
-            do {
+            s = ld_relaxed(&status[idx]);
+            while ((s >> 62) == 0) {
+                __nanosleep(20);
                 s = ld_relaxed(&status[idx]);
-            } while ((s >> 62) == 0);
+            }
         } else {
             s = kFlagPre | Op::identity;
         }

@@ -70,17 +70,29 @@ __global__ void __launch_bounds__(kNT) k_compact_raw(const unsigned *__restrict_
 
 // raw[i] = max(lcp_d[isa[i-1]], lcp_d[isa[i-1]+1]) for i in 1..n (1-based i),
 // with isa 0-based ranks and lcp_d[r] = lcp(sa[r-1], sa[r]), lcp_d[0] = lcp_d[n] = 0.
+// 8 consecutive slots per thread so 16 independent random loads are in flight.
 __global__ void k_raw_from_isa_lcp(const unsigned *__restrict__ isa, const unsigned *__restrict__ lcp_d,
                                    long long n, unsigned *__restrict__ raw) {
-    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i > n) return;
-    if (i == 0) {
-        raw[0] = 0;
-        return;
+    const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8;  // raw slots i0..i0+7
+    if (i0 > n) return;
+    unsigned r[8], a[8], b[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        long long i = i0 + j;
+        r[j] = (i >= 1 && i <= n) ? __ldg(isa + i - 1) : 0xffffffffu;
     }
-    unsigned r = __ldg(isa + i - 1);
-    unsigned a = __ldg(lcp_d + r), b = __ldg(lcp_d + r + 1);
-    raw[i] = a > b ? a : b;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (r[j] != 0xffffffffu) {
+            a[j] = __ldg(lcp_d + r[j]);
+            b[j] = __ldg(lcp_d + r[j] + 1);
+        } else {
+            a[j] = b[j] = 0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (i0 + j <= n) raw[i0 + j] = a[j] > b[j] ? a[j] : b[j];
 }
 
 // ---- int64 array-level kernels ------------------------------------------------
@@ -242,10 +254,11 @@ long long compact_from_raw(rs_ctx *c, long long n) {
     uint2 *llrc = (uint2 *)buf(c, B_LLRC, sizeof(uint2) * (size_t)(n + 8));
     unsigned long long *m_dev = (unsigned long long *)buf(c, B_SMALL, 4096);
     Scratch s = scratch(c, tiles);
-    RS_LAUNCH(c, k_compact_raw, (unsigned)tiles, kNT, 0, raw, n, llrc, m_dev, s.counter, s.status,
-              tiles);
+    RS_LAUNCH_B(c, 4.0 * (n + 1), k_compact_raw, (unsigned)tiles, kNT, 0, raw, n, llrc, m_dev, s.counter,
+                s.status, tiles);
     unsigned long long m = 0;
     fetch_small(c, &m, m_dev, sizeof(m));
+    add_bytes_last(c, 8.0 * (double)m);
     // zero the two pad entries after the last one (TMA staging reads them)
     RS_CUDA(cudaMemsetAsync(llrc + m, 0, sizeof(uint2) * 4, c->stream));
     return (long long)m;
@@ -258,7 +271,7 @@ size_t raw_slots(long long n) {
 
 void raw_from_rank_lcp(rs_ctx *c, long long n) {
     unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots(n));
-    RS_LAUNCH(c, k_raw_from_isa_lcp, grid_for(n + 1, 256), 256, 0, (const unsigned *)c->bufs[B_ISA].p,
+    RS_LAUNCH_B(c, 16.0 * n, k_raw_from_isa_lcp, grid_for((n + 8) / 8, 256), 256, 0, (const unsigned *)c->bufs[B_ISA].p,
               (const unsigned *)c->bufs[B_LCP].p, n, raw);
 }
 

@@ -19,8 +19,8 @@ namespace rsb {
 namespace {
 
 constexpr int kNT = 256;
-constexpr int kIPT = 16;
-constexpr int kTile = kNT * kIPT;  // 4096 pairs per tile
+constexpr int kIPT = 12;
+constexpr int kTile = kNT * kIPT;  // 3072 pairs per tile
 constexpr int kWarps = kNT / 32;
 constexpr int kRadix = 256;
 
@@ -61,11 +61,12 @@ struct SortSmem {
     unsigned vals[kTile];
     unsigned short warp_cnt[kWarps][kRadix];  // per-warp digit counts, then warp offsets
     unsigned tile_start[kRadix];              // exclusive scan of tile digit counts
+    unsigned hist[kRadix];                    // tile digit histogram
     unsigned long long global_base[kRadix];
     unsigned tile_id;
 };
 
-__global__ void __launch_bounds__(kNT) k_onesweep(const u64 *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
+__global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
                                                   u64 *__restrict__ keys_out, unsigned *__restrict__ vals_out,
                                                   long long count, int shift,
                                                   const unsigned long long *__restrict__ digit_base,
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(kNT) k_onesweep(const u64 *__restrict__ keys_i
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kWarps * kRadix; i += kNT) (&sm.warp_cnt[0][0])[i] = 0;
+    sm.hist[threadIdx.x] = 0;
     if (threadIdx.x == 0) sm.tile_id = atomicAdd(counter, 1u);
     __syncthreads();
     const long long tile = sm.tile_id;
@@ -90,6 +92,22 @@ __global__ void __launch_bounds__(kNT) k_onesweep(const u64 *__restrict__ keys_i
             v[i] = vals_in[idx];
         }
     }
+    // 1) tile digit histogram first, published right away (decoupled
+    //    look-back: successors can use this tile's aggregate while it is still
+    //    ranking, so the per-digit chains never wait on the ranking phase).
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        long long idx = base + i * 32 + lane;
+        if (idx < count) atomicAdd(&sm.hist[(unsigned)(k[i] >> shift) & 0xff], 1u);
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;
+        const unsigned run = sm.hist[d];
+        u64 *st = status + (size_t)tile * kRadix + d;
+        st_relaxed(st, (tile == 0 ? kFlagPre : kFlagAgg) | run);
+    }
+    // 2) stable ranking within each warp (warp-striped items: item-major, lane-minor)
     const unsigned lt_mask = (1u << lane) - 1;
 #pragma unroll
     for (int i = 0; i < kIPT; ++i) {
@@ -106,7 +124,7 @@ __global__ void __launch_bounds__(kNT) k_onesweep(const u64 *__restrict__ keys_i
         __syncwarp();
     }
     __syncthreads();
-    // per digit: warp exclusive offsets + tile total; publish + look back
+    // 3) per digit: warp exclusive offsets, tile-local digit start, look-back
     {
         const int d = threadIdx.x;  // kNT == kRadix
         unsigned run = 0;
@@ -116,29 +134,25 @@ __global__ void __launch_bounds__(kNT) k_onesweep(const u64 *__restrict__ keys_i
             sm.warp_cnt[w][d] = (unsigned short)run;
             run += c;
         }
-        // tile-local digit start: block exclusive scan over digits
         unsigned excl;
         __shared__ unsigned s_w[kNT / 32];
         block_exclusive_sum<kNT>(run, excl, s_w);
         sm.tile_start[d] = excl;
-        // decoupled look-back for this digit across tiles
-        u64 *st = status + (size_t)tile * kRadix + d;
         u64 prefix = 0;
-        if (tile == 0) {
-            st_relaxed(st, kFlagPre | run);
-        } else {
-            st_relaxed(st, kFlagAgg | run);
+        if (tile > 0) {
             long long t = tile - 1;
             while (true) {
                 u64 s;
-                do {
+                s = ld_relaxed(status + (size_t)t * kRadix + d);
+                while ((s >> 62) == 0) {
+                    __nanosleep(20);
                     s = ld_relaxed(status + (size_t)t * kRadix + d);
-                } while ((s >> 62) == 0);
+                }
                 prefix += s & kValMask;
                 if ((s >> 62) == 2) break;
                 --t;
             }
-            st_relaxed(st, kFlagPre | (prefix + run));
+            st_relaxed(status + (size_t)tile * kRadix + d, kFlagPre | (prefix + run));
         }
         sm.global_base[d] = digit_base[d] + prefix;
     }
@@ -178,7 +192,7 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
     unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * kRadix);
     RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
     unsigned hist_blocks = (unsigned)std::min<long long>((count + kNT * 16 - 1) / (kNT * 16), c->sm_count * 8);
-    RS_LAUNCH(c, k_histograms, hist_blocks, kNT, 0, keys, count, passes, hist);
+    RS_LAUNCH_B(c, 8.0 * count, k_histograms, hist_blocks, kNT, 0, keys, count, passes, hist);
     // Host needs the histograms to skip constant-digit passes.
     std::vector<unsigned long long> h((size_t)passes * kRadix);
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
@@ -199,7 +213,7 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
             if (h[(size_t)p * kRadix + d] == (unsigned long long)count) trivial = true;
         if (trivial) continue;
         Scratch s = scratch(c, tiles * kRadix);
-        RS_LAUNCH(c, k_onesweep, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout, vout, count, 8 * p,
+        RS_LAUNCH_B(c, 24.0 * count, k_onesweep, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout, vout, count, 8 * p,
                   hist + (size_t)p * kRadix, s.counter, s.status);
         std::swap(kin, kout);
         std::swap(vin, vout);

@@ -28,7 +28,8 @@ constexpr int kPPT = 8;
 constexpr int kG = kNT * kPPT;           // positions per tile
 constexpr int kCapC = kG + 1024;         // staged compact entries (uint2)
 constexpr int kCapR = 2 * kG + 2048;     // staged raw values (u32)
-constexpr int kStageBytes = 8 * kCapC + 64;
+constexpr int kStageBytes = 8 * kCapC + 128;
+constexpr int kQuerySmem = kStageBytes + 3 * 4 * kG;  // dynamic shared memory: stage + lo/hi/count
 
 // ---- TMA (1-D bulk copy) + mbarrier ------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -126,10 +127,14 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
                                                long long *__restrict__ out1, long long *__restrict__ flat,
                                                long long flat_cap, unsigned *counter, u64 *status,
                                                long long tiles, unsigned long long *total_out) {
-    __shared__ __align__(128) unsigned char s_stage[kStageBytes];
+    extern __shared__ __align__(128) unsigned char dsm[];
+    unsigned char *s_stage = dsm;
+    unsigned *s_lo = reinterpret_cast<unsigned *>(dsm + kStageBytes);  // window start per position
+    unsigned *s_hi = s_lo + kG;                                         // window end (exclusive)
+    unsigned *s_cnt = s_hi + kG;                                        // tie counts -> exclusive offsets
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ unsigned s_tile;
-    __shared__ u64 s_warp[kNT / 32];
+    __shared__ unsigned s_warp[kNT / 32];
     __shared__ u64 s_base;
 
     long long tile;
@@ -142,86 +147,72 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     }
     const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];
     const long long cnt = hi - lo;
+    const long long tile_k0 = kb + tile * kG;
+    const int npos = (int)((ke - tile_k0 + 1) < kG ? (ke - tile_k0 + 1) : kG);
+    const long long tile_k1 = tile_k0 + npos - 1;  // last position of the tile
 
-    // ---- stage the tile's candidate range [lo, hi) ----
+    // ---- stage the tile's candidate range [lo, hi) with one TMA bulk copy ----
     Cand<RAW> c;
     c.e = nullptr;
     c.r = nullptr;
     c.base = lo;
-    if (RAW) {
-        long long a = lo & ~3ll, b = (hi + 3) & ~3ll;
-        if (cnt > 0 && b - a <= kCapR) {
+    {
+        const int esz = RAW ? 4 : 8;
+        const long long align = 16 / esz;
+        long long a = lo & ~(align - 1), b = (hi + align - 1) & ~(align - 1);
+        const bool fits = cnt > 0 && b - a <= (RAW ? kCapR : kCapC);
+        if (fits) {
             if (threadIdx.x == 0) {
                 mbar_init(&s_bar, 1);
-                unsigned bytes = (unsigned)((b - a) * 4);
+                unsigned bytes = (unsigned)((b - a) * esz);
                 mbar_expect_tx(&s_bar, bytes);
-                tma_load_1d(s_stage, raw + a, bytes, &s_bar);
+                tma_load_1d(s_stage, RAW ? (const void *)(raw + a) : (const void *)(e + a), bytes, &s_bar);
             }
-            __syncthreads();
-            mbar_wait(&s_bar, 0);
-            c.r = reinterpret_cast<const unsigned *>(s_stage) + (lo - a);
-        } else {
-            c.r = raw + lo;
         }
-    } else {
-        long long a = lo & ~1ll, b = (hi + 1) & ~1ll;
-        if (cnt > 0 && b - a <= kCapC) {
-            if (threadIdx.x == 0) {
-                mbar_init(&s_bar, 1);
-                unsigned bytes = (unsigned)((b - a) * 8);
-                mbar_expect_tx(&s_bar, bytes);
-                tma_load_1d(s_stage, e + a, bytes, &s_bar);
-            }
-            __syncthreads();
+        // window bounds per position: every position's window is the
+        // contiguous candidate range [lo(k), hi(k)); lo(k) = first candidate
+        // with end >= k, hi(k) = #candidates with start <= k.  Both are
+        // nondecreasing, so each candidate fills the positions where it is
+        // the boundary -- O(tile + candidates), no searches.
+        for (int i = threadIdx.x; i < npos; i += kNT) {
+            s_lo[i] = (unsigned)cnt;
+            s_hi[i] = 0;
+        }
+        __syncthreads();
+        if (fits) {
             mbar_wait(&s_bar, 0);
-            c.e = reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
+            if (RAW) c.r = reinterpret_cast<const unsigned *>(s_stage) + (lo - a);
+            else c.e = reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
         } else {
-            c.e = e + lo;
+            if (RAW) c.r = raw + lo;
+            else c.e = e + lo;
         }
     }
+    for (long long t = threadIdx.x; t < cnt; t += kNT) {
+        long long ep = t ? c.end(t - 1) : tile_k0 - 1;
+        long long a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
+        long long b = c.end(t);
+        if (b > tile_k1) b = tile_k1;
+        for (long long k = a; k <= b; ++k) s_lo[k - tile_k0] = (unsigned)t;
+        long long sn = (t + 1 < cnt) ? c.start(t + 1) : tile_k1 + 1;
+        a = c.start(t) > tile_k0 ? c.start(t) : tile_k0;
+        b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
+        for (long long k = a; k <= b; ++k) s_hi[k - tile_k0] = (unsigned)(t + 1);
+    }
+    __syncthreads();
 
-    // ---- per-thread positions ----
-    const long long k0 = kb + tile * kG + (long long)threadIdx.x * kPPT;
+    // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
+    const long long slot0 = tile_k0 - kb + out_off;
     unsigned best[kPPT];
-    unsigned ties[kPPT];
-    long long bstart[kPPT];
-    long long w_lo = 0, w_hi = 0;
-    if (k0 <= ke) {
-        long long a = 0, b = cnt;  // first t with end >= k0
-        while (a < b) {
-            long long mid = (a + b) >> 1;
-            if (c.end(mid) >= k0) b = mid; else a = mid + 1;
-        }
-        w_lo = a;
-        if (RAW) {
-            w_hi = k0 - lo + 1;
-        } else {
-            a = w_lo;
-            b = cnt;
-            while (a < b) {
-                long long mid = (a + b) >> 1;
-                if (c.start(mid) <= k0) a = mid + 1; else b = mid;
-            }
-            w_hi = a;
-        }
-    }
-    unsigned my_total = 0;
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
-        const long long k = k0 + j;
+        const int p = threadIdx.x + j * kNT;
         best[j] = 0;
-        ties[j] = 0;
-        bstart[j] = -1;
-        if (k > ke) continue;
-        while (w_lo < cnt && c.end(w_lo) < k) ++w_lo;
-        if (RAW) {
-            w_hi = k - lo + 1;
-        } else {
-            while (w_hi < cnt && c.start(w_hi) <= k) ++w_hi;
-        }
+        if (p >= npos) continue;
+        const unsigned wl = s_lo[p], wh = s_hi[p];
         unsigned bl = 0, nt = 0;
         long long bs = -1;
-        for (long long t = w_lo; t < w_hi; ++t) {
+        for (unsigned t = wl; t < wh; ++t) {
             unsigned L = c.len(t);
             if (L > bl) {
                 bl = L;
@@ -232,20 +223,15 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
             }
         }
         best[j] = bl;
-        bstart[j] = bl ? bs : -1;
-        ties[j] = bl ? nt : 0;
-        my_total += ties[j];
-    }
-
-    if (!ALL) {
-#pragma unroll
-        for (int j = 0; j < kPPT; ++j) {
-            const long long k = k0 + j;
-            if (k > ke) break;
-            const long long slot = k - kb + out_off;
-            out0[slot] = bstart[j];
-            out1[slot] = best[j];
+        if (ALL) {
+            out0[slot0 + p] = bl;
+            s_cnt[p] = bl ? nt : 0;
+        } else {
+            out0[slot0 + p] = bl ? bs : -1;
+            out1[slot0 + p] = bl;
         }
+    }
+    if (!ALL) {
         if (tile == 0 && threadIdx.x == 0 && out_off) {
             out0[0] = -1;
             out1[0] = 0;
@@ -253,56 +239,56 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
         return;
     }
 
-    // ---- all ties: CSR offsets via block scan + look-back ----
-    u64 excl;
-    u64 block_total = block_exclusive_sum64<kNT>((u64)my_total, excl, s_warp);
+    // ---- all ties: exclusive scan of the tile's counts (position order) ----
+    __syncthreads();
+    unsigned mine[kPPT], msum = 0;
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x * kPPT + j;
+        mine[j] = p < npos ? s_cnt[p] : 0;
+        msum += mine[j];
+    }
+    unsigned excl;
+    const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, s_warp);
     if (threadIdx.x < 32) {
-        u64 base = lookback_warp(status, tile, block_total, OpSum());
+        u64 base = lookback_warp(status, tile, (u64)block_total, OpSum());
         if (threadIdx.x == 0) {
             s_base = base;
             if (tile == tiles - 1) *total_out = base + block_total;
         }
     }
-    __syncthreads();
-    u64 o = s_base + excl;
-    // window pointers again from the thread's first position
-    if (k0 <= ke) {
-        long long a = 0, b = cnt;
-        while (a < b) {
-            long long mid = (a + b) >> 1;
-            if (c.end(mid) >= k0) b = mid; else a = mid + 1;
-        }
-        w_lo = a;
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x * kPPT + j;
+        if (p < npos) s_cnt[p] = excl;
+        excl += mine[j];
     }
+    __syncthreads();
+    const u64 tile_base = s_base;
     if (tile == 0 && threadIdx.x == 0) {
         if (out_off) {
-            out0[0] = 0;   // lengths[0]
-            out1[0] = 0;   // offsets[0]
+            out0[0] = 0;  // lengths[0]
+            out1[0] = 0;  // offsets[0]
         }
-        out1[out_off] = 0;  // offsets[k=kb] (exclusive prefix of the first position)
+        out1[out_off] = 0;  // offsets of the first position
     }
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
-        const long long k = k0 + j;
-        if (k > ke) break;
-        const long long slot = k - kb + out_off;
-        out0[slot] = best[j];
-        out1[slot + 1] = (long long)(o + ties[j]);
-        if (ties[j]) {
-            while (w_lo < cnt && c.end(w_lo) < k) ++w_lo;
-            long long t = w_lo;
-            long long w = (long long)o;
-            const unsigned bl = best[j];
-            // walk forward until ties[j] starts are written (all lie in the window)
-            for (unsigned got = 0; got < ties[j]; ++t) {
-                if (c.len(t) == bl) {
-                    if (w < flat_cap) flat[w] = c.start(t);
-                    ++w;
-                    ++got;
-                }
+        const int p = threadIdx.x + j * kNT;
+        if (p >= npos) continue;
+        const unsigned ex = s_cnt[p];
+        const unsigned nxt = (p + 1 < npos) ? s_cnt[p + 1] : block_total;
+        out1[slot0 + 1 + p] = (long long)(tile_base + nxt);  // offsets[k+1] = inclusive prefix
+        const unsigned bl = best[j];
+        if (nxt == ex) continue;
+        u64 w = tile_base + ex;
+        const unsigned wl = s_lo[p], wh = s_hi[p];
+        for (unsigned t = wl; t < wh; ++t) {
+            if (c.len(t) == bl) {
+                if ((long long)w < flat_cap) flat[w] = c.start(t);
+                ++w;
             }
         }
-        o += ties[j];
     }
 }
 
@@ -323,15 +309,27 @@ void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     else
         RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds);
 
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA(cudaFuncSetAttribute(k_query<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
+        RS_CUDA(cudaFuncSetAttribute(k_query<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
+        RS_CUDA(cudaFuncSetAttribute(k_query<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
+        RS_CUDA(cudaFuncSetAttribute(k_query<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
+        attr = true;
+    }
     long long *out0 = (long long *)buf(c, B_OUT0, sizeof(long long) * (size_t)(n_slots + 1));
     long long *out1 = (long long *)buf(c, B_OUT1, sizeof(long long) * (size_t)(n_slots + 2));
     unsigned long long *tot = (unsigned long long *)buf(c, B_SMALL, 4096) + 2;
+    // algorithmic bytes: candidates read once (compact 8 B/entry, raw 4 B/slot),
+    // int64 outputs written once (leftmost 16 B/pos; all 16 B/pos + 8 B/tie).
+    const double cand_bytes = rawp ? 4.0 * (double)npos : 8.0 * (double)count;
+    const double qbytes = cand_bytes + 16.0 * (double)npos;
     if (!all) {
         if (rawp)
-            RS_LAUNCH(c, (k_query<true, false>), (unsigned)tiles, kNT, 0, d_e, d_raw, kb, ke, bounds, out_off,
+            RS_LAUNCH_B(c, qbytes, (k_query<true, false>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,
                       out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
         else
-            RS_LAUNCH(c, (k_query<false, false>), (unsigned)tiles, kNT, 0, d_e, d_raw, kb, ke, bounds,
+            RS_LAUNCH_B(c, qbytes, (k_query<false, false>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds,
                       out_off, out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
         c->out_mode = 0;
         return;
@@ -346,13 +344,14 @@ void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
         long long *flat = (long long *)buf(c, B_FLAT, sizeof(long long) * cap_slots);
         Scratch s = scratch(c, tiles);
         if (rawp)
-            RS_LAUNCH(c, (k_query<true, true>), (unsigned)tiles, kNT, 0, d_e, d_raw, kb, ke, bounds, out_off,
+            RS_LAUNCH_B(c, qbytes, (k_query<true, true>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,
                       out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot);
         else
-            RS_LAUNCH(c, (k_query<false, true>), (unsigned)tiles, kNT, 0, d_e, d_raw, kb, ke, bounds,
+            RS_LAUNCH_B(c, qbytes, (k_query<false, true>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds,
                       out_off, out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot);
         unsigned long long T = 0;
         fetch_small(c, &T, tot, sizeof(T));
+        add_bytes_last(c, 8.0 * (double)T);
         c->total = (long long)T;
         c->out_mode = 1;
         if ((size_t)T <= cap_slots) return;

@@ -1,0 +1,117 @@
+// scatter.cu -- L2-local permutation scatter: out[dest[i]] = val[i].
+//
+// Measured on B200 (ncu, profiles/): a random 4-byte store costs ~64 B of HBM
+// traffic (sector read-modify-write) and a random 4-byte load ~128 B, so the
+// two permutation steps of the path -- ISA[SA[r]] = r after the first sort
+// round and raw[SA[r]] = max(LCP[r], LCP[r+1]) -- were the slowest kernels.
+// Here they become two streaming passes:
+//   phase 1 (fused into the producer): (dest, val) pairs are appended to
+//     bucket dest >> S of a staging array.  dest is injective, so bucket b
+//     holds at most 2^S pairs and owns the fixed region [b*2^S, (b+1)*2^S);
+//     a block reserves its per-bucket run with one atomicAdd per bucket.
+//   phase 2 (k_bucket_apply): blocks walk the staging array bucket-major, so
+//     the few buckets in flight span a few MB of `out` and every random store
+//     merges in L2 before its line is written back once.
+// ~20 B of HBM traffic per element instead of ~64-128 B.
+#include "common.cuh"
+#include "scatter.cuh"
+
+namespace rsb {
+
+namespace {
+
+constexpr int kApplyNT = 256;
+constexpr int kApplyIPT = 16;
+
+__global__ void __launch_bounds__(kApplyNT) k_bucket_apply(const uint2 *__restrict__ stage,
+                                                           const unsigned *__restrict__ cursor, int shift,
+                                                           long long chunks_per_bucket,
+                                                           unsigned *__restrict__ out,
+                                                           const unsigned *__restrict__ stage2,
+                                                           unsigned *__restrict__ out2, int out2_shift) {
+    const long long b = blockIdx.x / chunks_per_bucket;
+    const long long chunk = blockIdx.x % chunks_per_bucket;
+    const long long count = cursor[b * kCursorStride];
+    const long long begin = chunk * (kApplyNT * kApplyIPT);
+    if (begin >= count) return;
+    const uint2 *src = stage + (b << shift);
+    uint2 v[kApplyIPT];
+#pragma unroll
+    for (int j = 0; j < kApplyIPT; ++j) {
+        long long i = begin + j * kApplyNT + threadIdx.x;
+        v[j] = i < count ? __ldcs(src + i) : make_uint2(0xffffffffu, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kApplyIPT; ++j)
+        if (v[j].x != 0xffffffffu) out[v[j].x] = v[j].y;
+    if (stage2) {
+        const unsigned *src2 = stage2 + (b << shift);
+#pragma unroll
+        for (int j = 0; j < kApplyIPT; ++j) {
+            long long i = begin + j * kApplyNT + threadIdx.x;
+            if (i < count) out2[v[j].x + out2_shift] = __ldcs(src2 + i);
+        }
+    }
+}
+
+// SA-order raw LLR (device-built structures): raw[sa[r] + 1] = max(lcp_d[r], lcp_d[r+1]).
+constexpr int kRNT = 256;
+constexpr int kRIPT = 8;
+__global__ void __launch_bounds__(kRNT) k_raw_sa_emit(const unsigned *__restrict__ sa, const unsigned *__restrict__ lcp_d,
+                                                     long long n, BucketEmit be) {
+    __shared__ unsigned short s_cnt[8 * kMaxBuckets];
+    __shared__ unsigned s_base[kMaxBuckets];
+    const long long r0 = (blockIdx.x * (long long)kRNT + threadIdx.x) * kRIPT;
+    unsigned dest[kRIPT], val[kRIPT];
+#pragma unroll
+    for (int j = 0; j < kRIPT; ++j) {
+        long long r = r0 + j;
+        if (r < n) {
+            dest[j] = sa[r] + 1;
+            unsigned a = lcp_d[r], c = lcp_d[r + 1];
+            val[j] = a > c ? a : c;
+        } else {
+            dest[j] = 0xffffffffu;
+        }
+    }
+    bucket_emit<kRIPT>(be, dest, val, s_cnt, s_base);
+}
+
+}  // namespace
+
+BucketEmit bucket_setup(rs_ctx *c, long long n_out, int slot, bool two) {
+    // <= 256 buckets: a block's items spread over few buckets (long runs), and
+    // the buckets in flight during phase 2 cover a few MB of `out` (L2-resident).
+    int shift = 12;
+    while (((n_out + (1ll << shift) - 1) >> shift) > kMaxBuckets && shift < 30) ++shift;
+    long long nb = (n_out + (1ll << shift) - 1) >> shift;
+    if (nb < 1) nb = 1;
+    if (nb > kMaxBuckets) fail(RS_EINVAL, "too many scatter buckets");
+    uint2 *stage = (uint2 *)buf(c, slot == 0 ? B_T2 : B_T3, sizeof(uint2) * (size_t)(nb << shift));
+    unsigned *cur = (unsigned *)buf(c, B_CURSOR, sizeof(unsigned) * 2 * kMaxBuckets * kCursorStride) +
+                    (size_t)slot * kMaxBuckets * kCursorStride;
+    RS_CUDA(cudaMemsetAsync(cur, 0, sizeof(unsigned) * (size_t)nb * kCursorStride, c->stream));
+    unsigned *stage2 = two ? (unsigned *)buf(c, slot == 0 ? B_T4 : B_T5, sizeof(unsigned) * (size_t)(nb << shift))
+                           : nullptr;
+    return BucketEmit{stage, cur, shift, nb, stage2};
+}
+
+void bucket_apply(rs_ctx *c, const BucketEmit &be, unsigned *out, long long elems, unsigned *out2,
+                  int out2_shift) {
+    long long per_block = kApplyNT * kApplyIPT;
+    long long chunks = ((1ll << be.shift) + per_block - 1) / per_block;
+    RS_LAUNCH_B(c, (out2 ? 20.0 : 12.0) * (double)elems, k_bucket_apply, (unsigned)(be.nb * chunks), kApplyNT, 0,
+                be.stage, be.cursor, be.shift, chunks, out, out2 ? be.stage2 : nullptr, out2, out2_shift);
+}
+
+// raw (B_RAW, 1-based u32) from device-built SA + SA-order LCP, via the bucketed scatter.
+void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n) {
+    unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots_n);
+    RS_CUDA(cudaMemsetAsync(raw, 0, sizeof(unsigned), c->stream));
+    BucketEmit be = bucket_setup(c, n + 1, 0);
+    RS_LAUNCH_B(c, 16.0 * n, k_raw_sa_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0,
+                (const unsigned *)c->bufs[B_SA].p, (const unsigned *)c->bufs[B_LCP].p, n, be);
+    bucket_apply(c, be, raw, n);
+}
+
+}  // namespace rsb

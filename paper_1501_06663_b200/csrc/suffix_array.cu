@@ -5,25 +5,33 @@
 //
 // B200 design (prefix doubling with group-head ranks, Larsson-Sadakane style):
 //   round 0: every suffix gets a packed key of its first K symbols, each an
-//            order-preserving code 1..sigma (0 = past the end) of b bits,
-//            K = floor(64 / b)  (DNA: b = 3, K = 21; sigma<=127: K = 9; bytes: K = 7).
+//            order-preserving code 1..sigma (0 = past the end) of b bits.
+//            K is the largest count that fits the fewest 8-bit radix passes
+//            while sigma^K >= 16 n (DNA at 256 Mi: b = 3, K = 16, 6 passes).
 //            One LSD radix sort of (key, position) pairs gives the SA order.
-//   k_update: SA/ISA write-back, ISA = SA index of the suffix's group head
-//            (single-pass max-scan with look-back) and compaction of the
-//            still-unsorted positions (sum-scan with look-back) in ONE kernel.
+//   k_update: SA write-back, ISA = SA slot of the suffix's group head
+//            (max-scan) and compaction of the still-unsorted slots (sum-scan),
+//            both through ONE decoupled look-back.  In round 0 it also emits
+//            the LCP of adjacent suffixes straight from their keys (exact
+//            when the keys differ) and each suffix's raw-LLR candidate
+//            max(LCP to predecessor, LCP to successor); ISA and raw go to text
+//            order through the bucketed scatter (scatter.cu).
 //   round r>=1 (h = K * 2^(r-1)): only unsorted suffixes get a key
 //            (ISA[i], ISA[i+h]+1 or 0 past the end) and are re-sorted; their
 //            groups occupy the same SA slots, so results write straight back.
 //   Rank = ISA (ranks are the final group heads), inversion is free.
-//   LCP: Phi array (scatter), PLCP by Kasai's carry over text-order chunks
-//   with 8-byte word compares, then LCP[r] = PLCP[SA[r]] (gather).
+//   LCP: pairs tied after round 0 (LCP >= K) are finished by direct word
+//   compares, which also fixes the raw LLR of their two suffixes.  When that
+//   would be expensive (repetitive text), Kasai over text-order chunks (PLCP
+//   via the Phi array) recomputes every LCP, and raw is rebuilt from SA order.
 // Device layouts: sa/isa u32[n] 0-based; lcp_d u32[n+2] with lcp_d[r] =
-// reference lcp[r+1] (lcp_d[0] = lcp_d[n] = 0).
+// reference lcp[r+1] (lcp_d[0] = lcp_d[n] = 0); raw u32 1-based (raw[0] = 0).
 #include <algorithm>
 #include <cmath>
 #include <vector>
 
 #include "common.cuh"
+#include "scatter.cuh"
 
 namespace rsb {
 
@@ -32,10 +40,18 @@ size_t raw_slots(long long n);
 namespace {
 
 constexpr unsigned kNone = 0xffffffffu;
+constexpr unsigned kLcpUnknown = 0xfffffffeu;
 
 struct CodeTable {
     unsigned short code[256];  // 1..sigma; sigma may be 256, so 9 bits
 };
+
+__device__ __forceinline__ u64 load8(const unsigned char *t, long long p) {
+    const u64 *w = reinterpret_cast<const u64 *>(t + (p & ~7ll));
+    unsigned sh = (unsigned)(p & 7) * 8;
+    u64 lo = __ldg(w), hi = __ldg(w + 1);
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+}
 
 __global__ void k_byte_hist(const unsigned char *__restrict__ text, long long n,
                             unsigned long long *__restrict__ hist) {
@@ -68,7 +84,7 @@ __global__ void __launch_bounds__(256) k_init_keys(const unsigned char *__restri
     vals[i] = (unsigned)i;
 }
 
-// Round r >= 1 keys for the unsorted positions P[0..U).
+// Round r >= 1 keys for the unsorted slots P[0..U).
 __global__ void k_make_keys(const unsigned *__restrict__ P, long long U, const unsigned *__restrict__ sa,
                             const unsigned *__restrict__ isa, long long n, long long h,
                             u64 *__restrict__ keys, unsigned *__restrict__ vals) {
@@ -85,29 +101,50 @@ constexpr int kUNT = 256;
 constexpr int kUIPT = 8;
 constexpr int kUTile = kUNT * kUIPT;
 
+__device__ __forceinline__ unsigned key_lcp(u64 a, u64 b, int code_bits, int key_bits) {
+    u64 x = a ^ b;
+    return x ? (unsigned)((__clzll((long long)x) - (64 - key_bits)) / code_bits) : kLcpUnknown;
+}
+
 // Write back one sorted run of (key, suffix) pairs occupying SA slots Pos(t)
-// (P[t], or t when P is null): sa[Pos(t)] = suffix, isa[suffix] = SA slot of
-// its new group head, and the positions still in non-singleton groups are
-// compacted into P_next.
+// (P[t], or t itself in round 0 when P is null): sa[Pos(t)] = suffix,
+// isa[suffix] = SA slot of its new group head, and the slots still in
+// non-singleton groups are compacted into P_next.
 __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, const unsigned *__restrict__ vals,
                                                  const unsigned *__restrict__ P, long long U,
                                                  unsigned *__restrict__ sa, unsigned *__restrict__ isa,
-                                                 unsigned *__restrict__ P_next,
-                                                 unsigned long long *U_next, unsigned *counter,
-                                                 u64 *status_max, u64 *status_sum, long long tiles) {
+                                                 unsigned *__restrict__ P_next, unsigned long long *U_next,
+                                                 unsigned *counter, u64 *status, long long tiles,
+                                                 unsigned *__restrict__ lcp_d, int code_bits, int key_bits,
+                                                 BucketEmit be) {
     __shared__ unsigned s_tile;
     __shared__ u64 s_warp[kUNT / 32];
     __shared__ unsigned s_warp32[kUNT / 32];
     __shared__ u64 s_head_prefix;
     __shared__ u64 s_base;
+    __shared__ __align__(16) unsigned s_stage[kUTile];
+    __shared__ unsigned short s_bcnt[8 * kMaxBuckets];
+    __shared__ unsigned s_bbase[kMaxBuckets];
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
     __syncthreads();
     const long long tile = s_tile;
     const int lane = threadIdx.x & 31;
     const long long t0 = tile * kUTile + (long long)threadIdx.x * kUIPT;
+    const long long tile_t0 = tile * kUTile;
+    const int tile_n = (int)((U - tile_t0) < kUTile ? (U - tile_t0) : kUTile);
     u64 k[kUIPT];
+    if (t0 + kUIPT <= U) {
+        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(keys + t0);
 #pragma unroll
-    for (int j = 0; j < kUIPT; ++j) k[j] = (t0 + j < U) ? keys[t0 + j] : ~0ull;
+        for (int j = 0; j < kUIPT / 2; ++j) {
+            ulonglong2 q = p[j];
+            k[2 * j] = q.x;
+            k[2 * j + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kUIPT; ++j) k[j] = (t0 + j < U) ? keys[t0 + j] : ~0ull;
+    }
     u64 kprev = __shfl_up_sync(0xffffffffu, k[kUIPT - 1], 1);
     u64 knext = __shfl_down_sync(0xffffffffu, k[0], 1);
     if (lane == 0) kprev = (t0 > 0 && t0 - 1 < U) ? keys[t0 - 1] : 0;
@@ -119,7 +156,6 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
         newf[j] = (t == 0) || (k[j] != (j ? k[j - 1] : kprev));
     }
     newf[kUIPT] = (t0 + kUIPT >= U) || (knext != k[kUIPT - 1]);
-    // last valid element's successor flag
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j)
         if (t0 + j + 1 == U) newf[j + 1] = true;
@@ -130,6 +166,7 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) {
         long long t = t0 + j;
+        pos[j] = 0;
         if (t < U) {
             pos[j] = P ? P[t] : (unsigned)t;
             if (newf[j]) hmax = (u64)pos[j];
@@ -138,22 +175,19 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
             ucnt += un;
         }
     }
-    // heads: inclusive max-scan across the block, then look-back over tiles
     u64 incl;
-    u64 tile_max = block_inclusive_max64<kUNT>(hmax, incl, s_warp);
-    u64 excl_in_block = __shfl_up_sync(0xffffffffu, incl, 1);
-    // inclusive of previous thread within the block:
-    // (block_inclusive_max64 returned this thread's inclusive value; derive the
-    //  exclusive one for thread 0 of each warp from the warp totals.)
+    const u64 tile_max = block_inclusive_max64<kUNT>(hmax, incl, s_warp);
+    const u64 excl_in_block = __shfl_up_sync(0xffffffffu, incl, 1);
     unsigned excl_u;
-    unsigned utotal = block_exclusive_sum<kUNT>(ucnt, excl_u, s_warp32);
+    const unsigned utotal = block_exclusive_sum<kUNT>(ucnt, excl_u, s_warp32);
     if (threadIdx.x < 32) {
-        u64 hp = lookback_warp(status_max, tile, tile_max, OpMax());
-        u64 up = lookback_warp(status_sum, tile, (u64)utotal, OpSum());
+        // one look-back for both scans: heads (max) in the high half, the
+        // unsorted count (sum) in the low half
+        u64 both = lookback_warp(status, tile, (tile_max << 31) | (u64)utotal, OpMaxSum());
         if (threadIdx.x == 0) {
-            s_head_prefix = hp;
-            s_base = up;
-            if (tile == tiles - 1) *U_next = up + utotal;
+            s_head_prefix = both >> 31;
+            s_base = both & ((1ull << 31) - 1);
+            if (tile == tiles - 1) *U_next = s_base + utotal;
         }
     }
     __syncthreads();
@@ -161,21 +195,96 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
     u64 run = s_head_prefix;
     {
         const int warp = threadIdx.x >> 5;
-        u64 prev_incl;
-        if (lane > 0) prev_incl = excl_in_block;
-        else prev_incl = warp ? s_warp[warp - 1] : 0;
+        u64 prev_incl = (lane > 0) ? excl_in_block : (warp ? s_warp[warp - 1] : 0);
         if (threadIdx.x > 0 && prev_incl > run) run = prev_incl;
     }
     u64 o = s_base + excl_u;
+    unsigned vv[kUIPT], hh[kUIPT];
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) {
         long long t = t0 + j;
-        if (t >= U) break;
+        vv[j] = kNoDest;
+        hh[j] = 0;
+        if (t >= U) continue;
         if (newf[j]) run = pos[j];
         unsigned v = vals[t];
-        sa[pos[j]] = v;
-        isa[v] = (unsigned)run;
+        vv[j] = v;
+        hh[j] = (unsigned)run;
+        if (P) {
+            sa[pos[j]] = v;
+            isa[v] = (unsigned)run;
+        }
         if (unsorted >> j & 1) P_next[o++] = pos[j];
+    }
+    if (P) return;
+    // ---- round 0: SA slots are t itself -> coalesced stores through shared memory ----
+#pragma unroll
+    for (int j = 0; j < kUIPT; ++j) s_stage[threadIdx.x * kUIPT + j] = vv[j];
+    __syncthreads();
+    for (int i = threadIdx.x; i < tile_n; i += kUNT) sa[tile_t0 + i] = s_stage[i];
+    __syncthreads();
+    // LCP of adjacent suffixes from their packed K-symbol keys when they
+    // differ; kLcpUnknown (true LCP >= K) otherwise.
+    unsigned lk[kUIPT + 1];
+#pragma unroll
+    for (int j = 0; j < kUIPT; ++j) {
+        long long t = t0 + j;
+        lk[j] = (t > 0 && t < U) ? key_lcp(k[j], j ? k[j - 1] : kprev, code_bits, key_bits) : 0;
+        s_stage[threadIdx.x * kUIPT + j] = lk[j];
+    }
+    lk[kUIPT] = (t0 + kUIPT < U) ? key_lcp(knext, k[kUIPT - 1], code_bits, key_bits) : 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < tile_n; i += kUNT) lcp_d[tile_t0 + i] = s_stage[i];
+    // raw LLR candidate of each suffix: max(LCP with SA predecessor, with
+    // successor); still-unknown pairs count as 0 and are fixed by k_lcp_patch
+    // (every suffix of a tied group is next to one such pair).
+    unsigned rr[kUIPT];
+#pragma unroll
+    for (int j = 0; j < kUIPT; ++j) {
+        unsigned a = lk[j] == kLcpUnknown ? 0 : lk[j];
+        unsigned b = lk[j + 1] == kLcpUnknown ? 0 : lk[j + 1];
+        rr[j] = a > b ? a : b;
+    }
+    bucket_emit<kUIPT>(be, vv, hh, s_bcnt, s_bbase, rr);
+}
+
+// LCP of the adjacent suffixes at SA slots r-1, r, known to be >= K.
+__device__ __forceinline__ unsigned lcp_from_depth(const unsigned char *__restrict__ text,
+                                                   const unsigned *__restrict__ sa, long long n, long long K,
+                                                   long long r) {
+    long long a = sa[r - 1], b = sa[r];
+    long long lim = n - (a > b ? a : b);
+    long long h = K < lim ? K : lim;
+    while (h < lim) {
+        u64 x = load8(text, a + h) ^ load8(text, b + h);
+        if (x == 0) {
+            h += 8;
+        } else {
+            h += (__ffsll((long long)x) - 1) >> 3;
+            break;
+        }
+    }
+    return (unsigned)(h > lim ? lim : h);
+}
+
+// Adjacent pairs whose round-0 keys were equal: lcp >= K, finished by 8-byte
+// word compares from depth K.  The raw LLR of both suffixes of a patched pair
+// is recomputed here; a neighbouring pair that is itself still unknown is
+// computed redundantly (the same value its own thread writes), so threads
+// need no ordering.
+__global__ void k_lcp_patch(const unsigned char *__restrict__ text, const unsigned *__restrict__ sa, long long n,
+                            long long K, unsigned *__restrict__ lcp_d, unsigned *__restrict__ raw) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x + 1; r < n; r += stride) {
+        if (lcp_d[r] != kLcpUnknown) continue;
+        const unsigned h = lcp_from_depth(text, sa, n, K, r);
+        lcp_d[r] = h;
+        unsigned lp = lcp_d[r - 1];
+        if (lp == kLcpUnknown) lp = lcp_from_depth(text, sa, n, K, r - 1);
+        unsigned ln = lcp_d[r + 1];
+        if (ln == kLcpUnknown) ln = lcp_from_depth(text, sa, n, K, r + 1);
+        raw[sa[r - 1] + 1] = lp > h ? lp : h;
+        raw[sa[r] + 1] = h > ln ? h : ln;
     }
 }
 
@@ -184,13 +293,6 @@ __global__ void k_phi(const unsigned *__restrict__ sa, long long n, unsigned *__
     long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (j >= n) return;
     phi[sa[j]] = j ? sa[j - 1] : kNone;
-}
-
-__device__ __forceinline__ u64 load8(const unsigned char *t, long long p) {
-    const u64 *w = reinterpret_cast<const u64 *>(t + (p & ~7ll));
-    unsigned sh = (unsigned)(p & 7) * 8;
-    u64 lo = __ldg(w), hi = __ldg(w + 1);
-    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
 }
 
 // Kasai over text-order chunks: PLCP[i] = lcp(i, phi[i]); carry h-1 within a chunk.
@@ -239,12 +341,15 @@ void build_suffix_array(rs_ctx *c, long long n) {
     unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 4));
     unsigned *isa = (unsigned *)buf(c, B_ISA, sizeof(unsigned) * (size_t)(n + 4));
     c->sa_rounds = 0;
+    c->lcp_from_keys = false;
+    c->sa_device_built = false;
+    c->raw_from_round0 = false;
     if (n <= 0) return;
     // alphabet -> order-preserving codes 1..sigma
     unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * 256);
     RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 256, c->stream));
     unsigned hb = (unsigned)std::min<long long>((n + 256 * 64 - 1) / (256 * 64), c->sm_count * 4);
-    RS_LAUNCH(c, k_byte_hist, hb, 256, 0, text, n, hist);
+    RS_LAUNCH_B(c, 1.0 * n, k_byte_hist, hb, 256, 0, text, n, hist);
     std::vector<unsigned long long> h(256);
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * 256);
     CodeTable ct;
@@ -252,17 +357,34 @@ void build_suffix_array(rs_ctx *c, long long n) {
     for (int b = 0; b < 256; ++b) ct.code[b] = h[b] ? (unsigned short)(++sigma) : 0;
     int bits = 1;
     while ((1 << bits) < sigma + 1) ++bits;
-    int K = 64 / bits;
+    // Round-0 key length: all Kmax symbols that fit in 64 bits, unless fewer
+    // already separate i.i.d. text (sigma^K >= 16 n) with fewer 8-bit radix
+    // passes; the prefix-doubling rounds resolve whatever stays tied.
+    const int Kmax = 64 / bits;
+    int K = Kmax;
+    if (sigma >= 2) {
+        double need = std::log2((double)n) + 4.0;
+        int Kr = (int)std::ceil(need / std::log2((double)sigma));
+        if (Kr < Kmax) {
+            int kb = ((Kr * bits + 7) / 8) * 8;
+            K = std::min(Kmax, std::max(1, kb / bits));
+        }
+    }
+    c->sa_key_symbols = K;
 
-    u64 *k0 = (u64 *)buf(c, B_KEYS0, sizeof(u64) * (size_t)n);
-    u64 *k1 = (u64 *)buf(c, B_KEYS1, sizeof(u64) * (size_t)n);
+    u64 *k0 = (u64 *)buf(c, B_KEYS0, sizeof(u64) * (size_t)n + 16);
+    u64 *k1 = (u64 *)buf(c, B_KEYS1, sizeof(u64) * (size_t)n + 16);
     unsigned *v0 = (unsigned *)buf(c, B_VALS0, sizeof(unsigned) * (size_t)n);
     unsigned *v1 = (unsigned *)buf(c, B_VALS1, sizeof(unsigned) * (size_t)n);
     unsigned *Pa = (unsigned *)buf(c, B_T0, sizeof(unsigned) * (size_t)n);
     unsigned *Pb = (unsigned *)buf(c, B_T1, sizeof(unsigned) * (size_t)n);
     unsigned long long *u_dev = (unsigned long long *)buf(c, B_SMALL, 4096) + 4;
+    unsigned *lcp_d = (unsigned *)buf(c, B_LCP, sizeof(unsigned) * (size_t)(n + 4));
+    RS_CUDA(cudaMemsetAsync(lcp_d + n, 0, sizeof(unsigned) * 4, c->stream));
+    unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots(n));
+    RS_CUDA(cudaMemsetAsync(raw, 0, sizeof(unsigned), c->stream));
 
-    RS_LAUNCH(c, k_init_keys, grid_for(n, 256), 256, 0, text, n, ct, bits, K, k0, v0);
+    RS_LAUNCH_B(c, 13.0 * n, k_init_keys, grid_for(n, 256), 256, 0, text, n, ct, bits, K, k0, v0);
     u64 *ks;
     unsigned *vs;
     radix_sort_pairs(c, k0, k1, v0, v1, n, bits * K, &ks, &vs);
@@ -276,20 +398,29 @@ void build_suffix_array(rs_ctx *c, long long n) {
     while (true) {
         ++c->sa_rounds;
         long long tiles = (U + kUTile - 1) / kUTile;
-        Scratch s = scratch(c, 2 * tiles);
-        RS_LAUNCH(c, k_update, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, u_dev, s.counter, s.status,
-                  s.status + tiles, tiles);
+        Scratch s = scratch(c, tiles);
+        BucketEmit be{nullptr, nullptr, 0, 0, nullptr};
+        if (!P) be = bucket_setup(c, n, 0, true);
+        // round 0: 12 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
+        RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, k_update, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, u_dev,
+                    s.counter, s.status, tiles, P ? nullptr : lcp_d, bits, bits * K, be);
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
+        add_bytes_last(c, 4.0 * (double)un);
+        if (!P) bucket_apply(c, be, isa, n, raw, 1);
         U = (long long)un;
+        if (c->sa_rounds == 1) c->sa_unsorted_after_round0 = U;
         if (U == 0) break;
         if (depth >= n) fail(RS_ECUDA, "suffix sort did not converge");
         std::swap(Pa, Pb);  // Pb now holds the unsorted list
         P = Pb;
-        RS_LAUNCH(c, k_make_keys, grid_for(U, 256), 256, 0, P, U, sa, isa, n, depth, k0, v0);
+        RS_LAUNCH_B(c, 28.0 * U, k_make_keys, grid_for(U, 256), 256, 0, P, U, sa, isa, n, depth, k0, v0);
         radix_sort_pairs(c, k0, k1, v0, v1, U, rbits, &ks, &vs);
         depth *= 2;
     }
+    c->lcp_from_keys = true;
+    c->sa_final_depth = depth;
+    c->sa_device_built = true;
 }
 
 void build_lcp(rs_ctx *c, long long n) {
@@ -300,13 +431,24 @@ void build_lcp(rs_ctx *c, long long n) {
     }
     const unsigned char *text = (const unsigned char *)c->bufs[B_TEXT].p;
     const unsigned *sa = (const unsigned *)c->bufs[B_SA].p;
+    // Patch work is at most (tied suffixes) x (final depth / 8 + 1) word
+    // compares; take it when that is cheaper than a full Kasai pass.
+    double patch_work = (double)c->sa_unsorted_after_round0 * (1.0 + (double)c->sa_final_depth / 8.0);
+    if (c->lcp_from_keys && patch_work <= 2.0 * (double)n) {
+        unsigned blocks = (unsigned)std::min<long long>(grid_for(n, 256), (long long)c->sm_count * 16);
+        RS_LAUNCH_B(c, 4.0 * n, k_lcp_patch, blocks, 256, 0, text, sa, n, (long long)c->sa_key_symbols, lcp_d,
+                    (unsigned *)c->bufs[B_RAW].p);
+        c->raw_from_round0 = true;  // B_RAW is final
+        return;
+    }
+    c->raw_from_round0 = false;
     unsigned *phi = (unsigned *)buf(c, B_PHI, sizeof(unsigned) * (size_t)n);
     unsigned *plcp = (unsigned *)buf(c, B_PLCP, sizeof(unsigned) * (size_t)n);
-    RS_LAUNCH(c, k_phi, grid_for(n, 256), 256, 0, sa, n, phi);
+    RS_LAUNCH_B(c, 8.0 * n, k_phi, grid_for(n, 256), 256, 0, sa, n, phi);
     long long chunk = std::max<long long>(32, n >> 19);
     long long chunks = (n + chunk - 1) / chunk;
-    RS_LAUNCH(c, k_plcp, grid_for(chunks, 128), 128, 0, text, phi, n, chunk, plcp);
-    RS_LAUNCH(c, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
+    RS_LAUNCH_B(c, 10.0 * n, k_plcp, grid_for(chunks, 128), 128, 0, text, phi, n, chunk, plcp);
+    RS_LAUNCH_B(c, 12.0 * n, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
 }
 
 }  // namespace rsb
