@@ -175,6 +175,8 @@ int rs_set_compact_device(rs_ctx *ctx, int64_t m, int64_t n);
 /* cudaStream_t of the context (for torch.cuda.ExternalStream). */
 int rs_stream(rs_ctx *ctx, void **stream);
 int rs_query_shard(rs_ctx *ctx, int mode, int64_t lo, int64_t hi, int64_t *total);
+/* Add `base` (the ties of all earlier shards) to the shard's offsets on device. */
+int rs_shard_rebase(rs_ctx *ctx, int64_t base);
 /* D2H of the shard results (a, b, flat as described above). */
 int rs_fetch_shard(rs_ctx *ctx, int mode, int64_t *a, int64_t *b, int64_t *flat);
 

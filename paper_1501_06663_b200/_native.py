@@ -75,6 +75,7 @@ SIGNATURES = {
     "rs_set_compact_device": [_CTX, ctypes.c_int64, ctypes.c_int64],
     "rs_stream": [_CTX, ctypes.POINTER(_VP)],
     "rs_query_shard": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _I64P],
+    "rs_shard_rebase": [_CTX, ctypes.c_int64],
     "rs_fetch_shard": [_CTX, ctypes.c_int, _I64P, _I64P, _I64P],
 }
 _RESTYPES = {"rs_version": ctypes.c_char_p, "rs_last_error": ctypes.c_char_p}

@@ -14,6 +14,7 @@ namespace rsb {
 // defined in compact.cu / scan_query.cu
 size_t raw_slots(long long n);
 void split_llrc(rs_ctx *c, long long m, long long *d_starts, long long *d_lengths);
+void add_i64(rs_ctx *c, long long *d, long long count, long long add);
 void join_llrc(rs_ctx *c, const long long *d_starts, const long long *d_lengths, long long m, long long n);
 void validate_llrc(rs_ctx *c, long long m, long long n);
 void check_raw(rs_ctx *c, long long n);
@@ -820,6 +821,15 @@ int rs_query_shard(rs_ctx *c, int mode, int64_t lo, int64_t hi, int64_t *total) 
         c->shard_lo = lo;
         c->shard_hi = hi;
         if (total) *total = mode == RS_MODE_ALL ? c->total : 0;
+    });
+}
+
+int rs_shard_rebase(rs_ctx *c, int64_t base) {
+    return guarded(c, [&] {
+        if (c->out_mode != RS_MODE_ALL) fail(RS_ESTATE, "no all-ties shard results on device");
+        long long cnt = c->shard_hi - c->shard_lo;
+        add_i64(c, (long long *)c->bufs[B_OUT1].p, cnt + 1, base);
+        RS_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 

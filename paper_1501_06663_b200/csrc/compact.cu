@@ -196,6 +196,11 @@ __global__ void k_widen(const unsigned *__restrict__ in, long long *__restrict__
     out[i] = (long long)in[i] + add;
 }
 
+__global__ void k_add_i64(long long *__restrict__ a, long long count, long long add) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < count) a[i] += add;
+}
+
 __global__ void k_split_llrc(const uint2 *__restrict__ llrc, long long m, long long *__restrict__ starts,
                              long long *__restrict__ lengths) {
     long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -298,6 +303,11 @@ void narrow_i64_to_u32(rs_ctx *c, const long long *d_in, unsigned *d_out, long l
 void widen_u32_to_i64(rs_ctx *c, const unsigned *d_in, long long *d_out, long long count, long long add) {
     if (count <= 0) return;
     RS_LAUNCH(c, k_widen, grid_for(count, 256), 256, 0, d_in, d_out, count, add);
+}
+
+void add_i64(rs_ctx *c, long long *d, long long count, long long add) {
+    if (count <= 0 || add == 0) return;
+    RS_LAUNCH(c, k_add_i64, grid_for(count, 256), 256, 0, d, count, add);
 }
 
 void split_llrc(rs_ctx *c, long long m, long long *d_starts, long long *d_lengths) {

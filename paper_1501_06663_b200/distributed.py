@@ -1,5 +1,287 @@
-"""Multi-GPU sharded query (placeholder; filled in below in this round)."""
+"""Multi-GPU longest-repeat query on one box: one process per GPU.
+
+Positions are independent reads of immutable candidate arrays with disjoint
+output slots (engine.py:3-7), so the path shards by POSITION:
+
+1. rank 0 builds the suffix structures, raw LLR and the compact array LLRc of
+   the whole text on its GPU (the suffix sort is not sharded yet: SURVEY
+   8(f)#1 is the next row);
+2. LLRc (8 bytes per entry) is broadcast with NCCL over NVLink, straight
+   from/into the library's device buffers (zero-copy torch views);
+3. rank r answers the contiguous position shard [lo_r, hi_r) of
+   engine._chunks; its left halo -- the entries that start before lo_r but
+   still cover it (at most max LLR - 1 positions back, Lemma 2) -- needs no
+   extra exchange because every rank holds the global LLRc and the per-tile
+   windows are found by binary search over it;
+4. all-ties: the per-shard tie totals are all-gathered (one int64 each), each
+   rank rebases its CSR offsets on device, and the shards are gathered to rank
+   0 with NCCL point-to-point into the final reference-layout arrays.
+
+Only plumbing (device views, NCCL collectives, final D2H) lives here; every
+kernel is in librepeatscan_b200.so.  The host-side pieces (shard ranges, tie
+bases, CSR assembly) are backend-agnostic so they are tested with gloo on CPU.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+from paper_1501_06663_b200 import _native
 
 
-def bench_main(args):
-    raise NotImplementedError("multi-GPU bench not implemented yet")
+# ---------------------------------------------------------------------------------------
+# host-side logic (backend agnostic)
+# ---------------------------------------------------------------------------------------
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """1-based half-open position range of `rank` -- engine._chunks (engine.py:43-52)."""
+    total = n
+    parts = max(1, min(world, total)) if total > 0 else 1
+    if rank >= parts:
+        return n + 1, n + 1
+    base, extra = divmod(total, parts)
+    lo = 1 + rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def tie_bases(totals: list[int]) -> list[int]:
+    """Exclusive prefix of the per-shard tie totals (CSR base of each shard)."""
+    out, acc = [], 0
+    for t in totals:
+        out.append(acc)
+        acc += int(t)
+    return out
+
+
+def exchange_totals(total: int, group=None, device=None) -> list[int]:
+    """all_gather of one int64 per rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.tensor([int(total)], dtype=torch.int64, device=device)
+    parts = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return [int(p.item()) for p in parts]
+
+
+def gather_shards(n: int, mode: str, lo: int, hi: int, a, b, flat, total_all: int, base: int,
+                  group=None, device=None):
+    """Assemble the reference-layout arrays on rank 0 from every rank's shard.
+
+    a, b, flat are torch tensors of this rank's shard (leftmost: a=starts[cnt],
+    b=lengths[cnt]; all: a=lengths[cnt], b=offsets[cnt+1] already rebased,
+    flat=tie starts[T_r]).  Returns the full torch tensors on rank 0, else None.
+    """
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    cnt = hi - lo
+    if rank != 0:
+        if cnt > 0:
+            dist.send(a[:cnt].contiguous(), dst=0, group=group)
+            if mode == "all":
+                dist.send(b[1:cnt + 1].contiguous(), dst=0, group=group)  # offsets[k+1]
+                if flat is not None and flat.numel() > 0:
+                    dist.send(flat.contiguous(), dst=0, group=group)
+            else:
+                dist.send(b[:cnt].contiguous(), dst=0, group=group)
+        return None
+    kw = dict(dtype=torch.int64, device=device)
+    if mode == "leftmost":
+        starts = torch.empty(n + 1, **kw)
+        lengths = torch.empty(n + 1, **kw)
+        starts[0] = -1
+        lengths[0] = 0
+        starts[lo:hi] = a[:cnt]
+        lengths[lo:hi] = b[:cnt]
+        for r in range(1, world):
+            rlo, rhi = shard_range(n, world, r)
+            if rhi > rlo:
+                dist.recv(starts[rlo:rhi], src=r, group=group)
+                dist.recv(lengths[rlo:rhi], src=r, group=group)
+        return starts, lengths
+    lengths = torch.empty(n + 1, **kw)
+    offsets = torch.empty(n + 2, **kw)
+    flat_all = torch.empty(max(total_all, 0), **kw)
+    lengths[0] = 0
+    offsets[0] = 0
+    offsets[1] = 0
+    if cnt > 0:
+        lengths[lo:hi] = a[:cnt]
+        # b[0] is the exclusive base of the shard's first position; b[1:] are offsets[k+1]
+        offsets[lo + 1:hi + 1] = b[1:cnt + 1]
+        t0 = int(b[0].item()) if hasattr(b[0], "item") else int(b[0])
+        if flat is not None and flat.numel() > 0:
+            flat_all[t0:t0 + flat.numel()] = flat
+    for r in range(1, world):
+        rlo, rhi = shard_range(n, world, r)
+        if rhi <= rlo:
+            continue
+        dist.recv(lengths[rlo:rhi], src=r, group=group)
+        tmp = torch.empty(rhi - rlo, **kw)
+        dist.recv(tmp, src=r, group=group)
+        offsets[rlo + 1:rhi + 1] = tmp
+        s = int(offsets[rlo].item())
+        e = int(offsets[rhi].item())
+        if e > s:
+            dist.recv(flat_all[s:e], src=r, group=group)
+    return lengths, offsets, flat_all
+
+
+# ---------------------------------------------------------------------------------------
+# device path
+# ---------------------------------------------------------------------------------------
+class _CudaView:
+    """__cuda_array_interface__ view of a library device buffer (no copy)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _view(ctx: _native.Context, which: int, count: int, typestr: str, device):
+    import torch
+    itemsize = int(typestr[-1])
+    ptr = ctx.device_buffer(which, max(count, 1) * itemsize)
+    return torch.as_tensor(_CudaView(ptr, count, typestr), device=device)
+
+
+def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None,
+                          timings: dict | None = None):
+    """Distributed query.  `data` (uint8 text) is needed on rank 0 only.
+
+    Returns torch device tensors of the reference layout on rank 0
+    ((starts, lengths) or (lengths, offsets, flat)), None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev_index = torch.cuda.current_device()
+    device = torch.device("cuda", dev_index)
+    ctx = _native.context(dev_index)
+    t = {} if timings is None else timings
+    with ctx.lock:
+        # 1. rank 0: text -> SA -> LCP -> raw LLR -> LLRc on its GPU
+        meta = torch.zeros(2, dtype=torch.int64, device=device)
+        if rank == 0:
+            host = np.ascontiguousarray(data, dtype=np.uint8)
+            n = int(host.size)
+            ctx.call("rs_set_text", _native.u8(host), n)
+            m_arr = np.zeros(1, np.int64)
+            ctx.call("rs_get_compact_size", _native.i64(m_arr))
+            ctx.synchronize()
+            meta[0], meta[1] = n, int(m_arr[0])
+        dist.broadcast(meta, src=0, group=group)
+        n, m = int(meta[0].item()), int(meta[1].item())
+        # 2. LLRc broadcast, device buffer to device buffer (uint32 pairs)
+        llrc = _view(ctx, _native.BUF_LLRC, 2 * m + 8, "<i4", device)  # (start, len) u32 pairs, bit-cast
+        if m > 0:
+            dist.broadcast(llrc[:2 * m], src=0, group=group)
+        torch.cuda.synchronize(device)
+        if rank != 0:
+            ctx.call("rs_set_compact_device", m, n)
+        # 3. shard scan
+        lo, hi = shard_range(n, world, rank)
+        total = np.zeros(1, np.int64)
+        ctx.call("rs_query_shard", _native.MODE[mode], lo, hi, _native.i64(total))
+        cnt = hi - lo
+        if mode == "all":
+            totals = exchange_totals(int(total[0]), group, device)
+            bases = tie_bases(totals)
+            ctx.call("rs_shard_rebase", bases[rank])
+            T_all = sum(totals)
+            a = _view(ctx, _native.BUF_OUT0, cnt, "<i8", device)
+            b = _view(ctx, _native.BUF_OUT1, cnt + 1, "<i8", device)
+            f = _view(ctx, _native.BUF_FLAT, int(total[0]), "<i8", device)
+            ctx.synchronize()
+            out = gather_shards(n, mode, lo, hi, a, b, f, T_all, bases[rank], group, device)
+        else:
+            a = _view(ctx, _native.BUF_OUT0, cnt, "<i8", device)
+            b = _view(ctx, _native.BUF_OUT1, cnt, "<i8", device)
+            ctx.synchronize()
+            out = gather_shards(n, mode, lo, hi, a, b, None, 0, 0, group, device)
+        torch.cuda.synchronize(device)
+    return out
+
+
+def to_answers(out, mode: str):
+    """Rank-0 tensors -> reference dataclasses (one D2H each)."""
+    from paper_1501_06663_b200.query import AllAnswers, LeftmostAnswers
+    if mode == "leftmost":
+        s, l = out
+        return LeftmostAnswers(starts=s.cpu().numpy(), lengths=l.cpu().numpy())
+    l, o, f = out
+    return AllAnswers(lengths=l.cpu().numpy(), offsets=o.cpu().numpy(), flat_starts=f.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------------------
+# bench (torchrun, N > 1)
+# ---------------------------------------------------------------------------------------
+def bench_main(args) -> None:
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1501_06663_b200 import workloads
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    data = workloads.make(args.config, args.n) if rank == 0 else None
+    n = int(data.size) if rank == 0 else 0
+
+    def step():
+        return sharded_all_positions(data, "all")
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        out = step()
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    nn = torch.tensor([n], dtype=torch.int64, device="cuda")
+    dist.broadcast(nn, src=0)
+    n = int(nn.item())
+    # e2e: H2D of the text on rank 0 (inside rs_set_text) + final D2H of the CSR
+    e2e = []
+    for _ in range(max(1, args.steps)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = step()
+        res = to_answers(out, "all") if rank == 0 else None
+        torch.cuda.synchronize()
+        dist.barrier()
+        e2e.append(time.perf_counter() - t0)
+    if rank == 0:
+        T = int(res.flat_starts.size)
+        line = {
+            "metric": "positions/sec, all-longest-repeat query, n=256M DNA, 1/2/4/8 B200 vs CPU",
+            "value": n / (ms * 1e-3), "unit": "positions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
+            "data": "synthetic",
+            "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
+                       "parallelism": f"position shards x{world} (SA/LLRc on rank 0, NCCL broadcast)",
+                       "T": T},
+            "gpu_launches": None,
+            "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": n,
+                    "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T},
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -1,0 +1,89 @@
+"""Multi-rank host logic of the sharded query, on CPU with gloo (world size 2 and 3).
+
+Per-shard device results are stood in for by slices of the oracle's answer
+(tests may use the oracle); everything else -- shard ranges, the tie-total
+all_gather, CSR rebasing and the point-to-point gather into the reference
+layout -- is the production code of paper_1501_06663_b200.distributed.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1501_06663_b200 import distributed as D
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, data, q):
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = data.size
+        wl, wo, wf = oracle.all_positions(data, mode="all")
+        ls, ll = oracle.all_positions(data, mode="leftmost")
+        lo, hi = D.shard_range(n, world, rank)
+        cnt = hi - lo
+        # shard-local results as rs_query_shard produces them
+        a = torch.from_numpy(wl[lo:hi].copy())
+        local_off = wo[lo:hi + 1] - wo[lo]
+        f = torch.from_numpy(wf[wo[lo]:wo[hi]].copy())
+        totals = D.exchange_totals(int(f.numel()))
+        bases = D.tie_bases(totals)
+        b = torch.from_numpy(local_off + bases[rank])  # rs_shard_rebase
+        out = D.gather_shards(n, "all", lo, hi, a, b, f, sum(totals), bases[rank])
+        left = D.gather_shards(n, "leftmost", lo, hi, torch.from_numpy(ls[lo:hi].copy()),
+                               torch.from_numpy(ll[lo:hi].copy()), None, 0, 0)
+        if rank == 0:
+            ok = (np.array_equal(out[0].numpy(), wl) and np.array_equal(out[1].numpy(), wo)
+                  and np.array_equal(out[2].numpy(), wf) and np.array_equal(left[0].numpy(), ls)
+                  and np.array_equal(left[1].numpy(), ll))
+            q.put(("ok" if ok else "mismatch", cnt))
+        else:
+            assert out is None and left is None
+    except Exception as e:  # surface errors to the parent
+        q.put((f"error: {e!r}", rank))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gather_matches_full_answer(world):
+    from paper_1501_06663_b200 import workloads
+    data = workloads.planted_dna(5000, 7, family_len=40)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, data, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    status, _ = q.get(timeout=10)
+    assert status == "ok", status
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def test_shard_ranges_partition():
+    for n in (0, 1, 5, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            covered = []
+            for r in range(world):
+                lo, hi = D.shard_range(n, world, r)
+                assert 1 <= lo <= hi <= n + 1
+                covered += list(range(lo, hi))
+            assert covered == list(range(1, n + 1))
+    assert D.tie_bases([3, 0, 5]) == [0, 3, 3]

@@ -205,3 +205,78 @@ def test_kernels_launch_from_native_library():
     before = ctx.launches()
     rb.all_positions(rb.Text(workloads.iid_dna(10000, 1)), mode="all")
     assert ctx.launches() > before
+
+
+def test_shard_queries_assemble_to_full_answer():
+    # Device-side halo handling: each shard [lo, hi) is answered from the
+    # global compact array (rs_query_shard); stitched shards == full answer.
+    from paper_1501_06663_b200 import _native
+    from paper_1501_06663_b200 import distributed as D
+    for data in (workloads.planted_dna(300_000, 9, family_len=200),
+                 workloads.fibonacci_mutated(200_000, 5, rate=1e-3)):
+        n = data.size
+        want_l, want_o, want_f = oracle.all_positions(data, mode="all")
+        want_s, want_len = oracle.all_positions(data, mode="leftmost")
+        ctx = _native.context()
+        for world in (2, 3, 8):
+            lengths = np.zeros(n + 1, np.int64)
+            offsets = np.zeros(n + 2, np.int64)
+            flats, base = [], 0
+            starts = np.full(n + 1, -1, np.int64)
+            llen = np.zeros(n + 1, np.int64)
+            for r in range(world):
+                lo, hi = D.shard_range(n, world, r)
+                with ctx.lock:
+                    ctx.call("rs_set_text", _native.u8(data), n)
+                    m = np.zeros(1, np.int64)
+                    ctx.call("rs_get_compact_size", _native.i64(m))
+                    tot = np.zeros(1, np.int64)
+                    ctx.call("rs_query_shard", 1, lo, hi, _native.i64(tot))
+                    ctx.call("rs_shard_rebase", base)
+                    a = np.zeros(hi - lo, np.int64)
+                    b = np.zeros(hi - lo + 1, np.int64)
+                    f = np.zeros(int(tot[0]), np.int64)
+                    ctx.call("rs_fetch_shard", 1, _native.i64(a), _native.i64(b), _native.i64(f))
+                    ctx.call("rs_query_shard", 0, lo, hi, _native.i64(tot))
+                    sa_ = np.zeros(hi - lo, np.int64)
+                    sl_ = np.zeros(hi - lo, np.int64)
+                    ctx.call("rs_fetch_shard", 0, _native.i64(sa_), _native.i64(sl_), _native.i64(f[:0]))
+                lengths[lo:hi] = a
+                offsets[lo + 1:hi + 1] = b[1:]
+                assert b[0] == base
+                flats.append(f)
+                base += f.size
+                starts[lo:hi] = sa_
+                llen[lo:hi] = sl_
+            assert np.array_equal(lengths, want_l) and np.array_equal(offsets, want_o), world
+            assert np.array_equal(np.concatenate(flats), want_f), world
+            assert np.array_equal(starts, want_s) and np.array_equal(llen, want_len), world
+
+
+def test_distributed_single_rank_nccl():
+    # sharded_all_positions end to end through torch.distributed/NCCL device
+    # views of the library buffers (world size 1 on the one GPU available).
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1501_06663_b200 import distributed as D
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        data = workloads.planted_dna(200_000, 3, family_len=100)
+        out = D.sharded_all_positions(data, "all")
+        res = D.to_answers(out, "all")
+        wl, wo, wf = oracle.all_positions(data, mode="all")
+        assert np.array_equal(res.lengths, wl) and np.array_equal(res.offsets, wo)
+        assert np.array_equal(res.flat_starts, wf)
+        out = D.sharded_all_positions(data, "leftmost")
+        res = D.to_answers(out, "leftmost")
+        ws, wln = oracle.all_positions(data, mode="leftmost")
+        assert np.array_equal(res.starts, ws) and np.array_equal(res.lengths, wln)
+    finally:
+        dist.destroy_process_group()
