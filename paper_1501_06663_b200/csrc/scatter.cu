@@ -59,8 +59,7 @@ constexpr int kRNT = 256;
 constexpr int kRIPT = 8;
 __global__ void __launch_bounds__(kRNT) k_raw_sa_emit(const unsigned *__restrict__ sa, const unsigned *__restrict__ lcp_d,
                                                      long long n, BucketEmit be) {
-    __shared__ unsigned short s_cnt[8 * kMaxBuckets];
-    __shared__ unsigned s_base[kMaxBuckets];
+    __shared__ EmitSmem<kRNT, kRIPT> sm;
     const long long r0 = (blockIdx.x * (long long)kRNT + threadIdx.x) * kRIPT;
     unsigned dest[kRIPT], val[kRIPT];
 #pragma unroll
@@ -74,7 +73,7 @@ __global__ void __launch_bounds__(kRNT) k_raw_sa_emit(const unsigned *__restrict
             dest[j] = 0xffffffffu;
         }
     }
-    bucket_emit<kRIPT>(be, dest, val, s_cnt, s_base);
+    bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
 }
 
 }  // namespace

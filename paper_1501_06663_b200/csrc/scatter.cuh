@@ -18,19 +18,31 @@ struct BucketEmit {
     unsigned *stage2;   // optional second value per pair (same slot), or null
 };
 
+// Shared memory for bucket_emit with NT threads x IPT items.
+template <int NT, int IPT>
+struct EmitSmem {
+    unsigned short cnt[8][kMaxBuckets];  // per-warp bucket counts -> warp offsets
+    unsigned bstart[kMaxBuckets];        // block-local start of each bucket run
+    unsigned gbase[kMaxBuckets];         // global slot reserved for the block's run
+    unsigned dest[NT * IPT];             // items exchanged into bucket order
+    unsigned val[NT * IPT];
+    unsigned val2[NT * IPT];
+    unsigned warp_tot[NT / 32];
+};
+
 // Phase 1, called by every thread of a 256-thread block (contains
-// __syncthreads): append this thread's IPT (dest, val) pairs (dest ==
-// kNoDest: none) to their buckets.  Ranking is warp-synchronous
-// (match_any + per-warp counters, no shared-memory atomics); one global
-// atomicAdd per (block, bucket) reserves the block's run.
-// s_cnt must hold 8 * 256 u16 counters, s_base 256 u32.
-template <int IPT>
+// __syncthreads): append this thread's IPT (dest, val[, val2]) items (dest ==
+// kNoDest: none) to their buckets.  Warp-synchronous ranking (match_any, no
+// shared-memory atomics), one global atomicAdd per (block, bucket), and an
+// exchange through shared memory so each bucket's run is written by
+// consecutive threads (coalesced) instead of one scattered store per item.
+template <int NT, int IPT>
 __device__ __forceinline__ void bucket_emit(const BucketEmit &be, const unsigned *dest, const unsigned *val,
-                                            unsigned short *s_cnt, unsigned *s_base,
-                                            const unsigned *val2 = nullptr) {
+                                            EmitSmem<NT, IPT> &sm, const unsigned *val2 = nullptr) {
+    static_assert(NT == 256, "one thread per bucket");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned short *wc = s_cnt + warp * 256;
-    for (int i = lane; i < 256; i += 32) wc[i] = 0;
+    unsigned short *wc = sm.cnt[warp];
+    for (int i = lane; i < kMaxBuckets; i += 32) wc[i] = 0;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1;
     unsigned short rank[IPT];
@@ -49,26 +61,47 @@ __device__ __forceinline__ void bucket_emit(const BucketEmit &be, const unsigned
     }
     __syncthreads();
     {
-        const int b = threadIdx.x;  // one thread per bucket (nb <= 256)
-        if (b < be.nb) {
-            unsigned run = 0;
+        const int b = threadIdx.x;
+        unsigned run = 0;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const unsigned c = s_cnt[w * 256 + b];
-                s_cnt[w * 256 + b] = (unsigned short)run;
-                run += c;
-            }
-            if (run) s_base[b] = atomicAdd(&be.cursor[b * kCursorStride], run);
+        for (int w = 0; w < 8; ++w) {
+            const unsigned c = sm.cnt[w][b];
+            sm.cnt[w][b] = (unsigned short)run;
+            run += c;
         }
+        // block-exclusive scan of the bucket totals (bucket order)
+        unsigned x = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) sm.warp_tot[warp] = x;
+        __syncthreads();
+        unsigned wbase = 0;
+        for (int w = 0; w < warp; ++w) wbase += sm.warp_tot[w];
+        sm.bstart[b] = wbase + x - run;
+        if (b < be.nb && run) sm.gbase[b] = atomicAdd(&be.cursor[b * kCursorStride], run);
     }
     __syncthreads();
+    unsigned total = 0;
+    for (int w = 0; w < NT / 32; ++w) total += sm.warp_tot[w];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         if (dest[j] == kNoDest) continue;
         const unsigned b = dest[j] >> be.shift;
-        const long long slot = ((long long)b << be.shift) + s_base[b] + wc[b] + rank[j];
-        be.stage[slot] = make_uint2(dest[j], val[j]);
-        if (val2) be.stage2[slot] = val2[j];
+        const unsigned p = sm.bstart[b] + wc[b] + rank[j];
+        sm.dest[p] = dest[j];
+        sm.val[p] = val[j];
+        if (val2) sm.val2[p] = val2[j];
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < total; i += NT) {
+        const unsigned d = sm.dest[i];
+        const unsigned b = d >> be.shift;
+        const long long slot = ((long long)b << be.shift) + sm.gbase[b] + (i - sm.bstart[b]);
+        be.stage[slot] = make_uint2(d, sm.val[i]);
+        if (val2) be.stage2[slot] = sm.val2[i];
     }
 }
 

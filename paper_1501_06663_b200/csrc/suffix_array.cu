@@ -110,24 +110,21 @@ __device__ __forceinline__ unsigned key_lcp(u64 a, u64 b, int code_bits, int key
 // (P[t], or t itself in round 0 when P is null): sa[Pos(t)] = suffix,
 // isa[suffix] = SA slot of its new group head, and the slots still in
 // non-singleton groups are compacted into P_next.
+template <bool REDUCE>
 __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, const unsigned *__restrict__ vals,
                                                  const unsigned *__restrict__ P, long long U,
                                                  unsigned *__restrict__ sa, unsigned *__restrict__ isa,
-                                                 unsigned *__restrict__ P_next, unsigned long long *U_next,
-                                                 unsigned *counter, u64 *status, long long tiles,
+                                                 unsigned *__restrict__ P_next, u64 *__restrict__ tile_agg,
+                                                 const u64 *__restrict__ tile_prefix,
                                                  unsigned *__restrict__ lcp_d, int code_bits, int key_bits,
                                                  BucketEmit be) {
-    __shared__ unsigned s_tile;
     __shared__ u64 s_warp[kUNT / 32];
     __shared__ unsigned s_warp32[kUNT / 32];
     __shared__ u64 s_head_prefix;
     __shared__ u64 s_base;
-    __shared__ __align__(16) unsigned s_stage[kUTile];
-    __shared__ unsigned short s_bcnt[8 * kMaxBuckets];
-    __shared__ unsigned s_bbase[kMaxBuckets];
-    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
-    __syncthreads();
-    const long long tile = s_tile;
+    __shared__ EmitSmem<kUNT, kUIPT> s_emit;
+    unsigned *s_stage = s_emit.val;  // reused before the emit
+    const long long tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
     const long long t0 = tile * kUTile + (long long)threadIdx.x * kUIPT;
     const long long tile_t0 = tile * kUTile;
@@ -180,15 +177,15 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
     const u64 excl_in_block = __shfl_up_sync(0xffffffffu, incl, 1);
     unsigned excl_u;
     const unsigned utotal = block_exclusive_sum<kUNT>(ucnt, excl_u, s_warp32);
-    if (threadIdx.x < 32) {
-        // one look-back for both scans: heads (max) in the high half, the
-        // unsorted count (sum) in the low half
-        u64 both = lookback_warp(status, tile, (tile_max << 31) | (u64)utotal, OpMaxSum());
-        if (threadIdx.x == 0) {
-            s_head_prefix = both >> 31;
-            s_base = both & ((1ull << 31) - 1);
-            if (tile == tiles - 1) *U_next = s_base + utotal;
-        }
+    if (REDUCE) {
+        // pass 1 of reduce-then-scan: this tile's (max head, unsorted count)
+        if (threadIdx.x == 0) tile_agg[tile] = (tile_max << 31) | (u64)utotal;
+        return;
+    }
+    if (threadIdx.x == 0) {
+        const u64 both = tile_prefix[tile];  // exclusive (max, sum) over earlier tiles
+        s_head_prefix = both >> 31;
+        s_base = both & ((1ull << 31) - 1);
     }
     __syncthreads();
     // exclusive max for this thread = max(tile prefix, inclusive value of previous thread)
@@ -245,7 +242,48 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
         unsigned b = lk[j + 1] == kLcpUnknown ? 0 : lk[j + 1];
         rr[j] = a > b ? a : b;
     }
-    bucket_emit<kUIPT>(be, vv, hh, s_bcnt, s_bbase, rr);
+    __syncthreads();
+    bucket_emit<kUNT, kUIPT>(be, vv, hh, s_emit, rr);
+}
+
+// Pass 2 of reduce-then-scan over the k_update tiles: exclusive OpMaxSum
+// prefix per tile (one block; a few hundred thousand tiles at most) and the
+// total unsorted count.
+__global__ void __launch_bounds__(1024) k_tile_scan(const u64 *__restrict__ agg, long long tiles,
+                                                    u64 *__restrict__ prefix, unsigned long long *U_next) {
+    __shared__ u64 s_w[32];
+    const OpMaxSum op;
+    const long long per = (tiles + 1023) / 1024;
+    const long long a = threadIdx.x * per, b = a + per < tiles ? a + per : tiles;
+    u64 acc = 0;
+    for (long long t = a; t < b; ++t) acc = op(acc, agg[t]);
+    // block exclusive scan of acc with op
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u64 x = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = op(x, y);
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        u64 w = s_w[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w = op(w, y);
+        }
+        s_w[lane] = w;
+    }
+    __syncthreads();
+    u64 run = op(warp ? s_w[warp - 1] : 0ull, __shfl_up_sync(0xffffffffu, x, 1));
+    if (lane == 0) run = warp ? s_w[warp - 1] : 0ull;
+    for (long long t = a; t < b; ++t) {
+        prefix[t] = run;
+        run = op(run, agg[t]);
+    }
+    if (threadIdx.x == 1023) *U_next = s_w[31] & ((1ull << 31) - 1);
 }
 
 // LCP of the adjacent suffixes at SA slots r-1, r, known to be >= K.
@@ -398,12 +436,17 @@ void build_suffix_array(rs_ctx *c, long long n) {
     while (true) {
         ++c->sa_rounds;
         long long tiles = (U + kUTile - 1) / kUTile;
-        Scratch s = scratch(c, tiles);
+        u64 *tagg = (u64 *)buf(c, B_BOUNDS, sizeof(u64) * 2 * (size_t)(tiles + 1));
+        u64 *tpre = tagg + tiles + 1;
         BucketEmit be{nullptr, nullptr, 0, 0, nullptr};
         if (!P) be = bucket_setup(c, n, 0, true);
+        // reduce-then-scan instead of a look-back: the heavy pass never waits
+        RS_LAUNCH_B(c, 8.0 * U, k_update<true>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, tagg, tpre,
+                    lcp_d, bits, bits * K, be);
+        RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
         // round 0: 12 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
-        RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, k_update, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, u_dev,
-                    s.counter, s.status, tiles, P ? nullptr : lcp_d, bits, bits * K, be);
+        RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, k_update<false>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa,
+                    tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
         add_bytes_last(c, 4.0 * (double)un);
