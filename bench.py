@@ -223,11 +223,11 @@ def run_single(args) -> None:
             ctx.call("rs_clear_derived")
             ctx.call("rs_query", 1, 1, _native.i64(total))
 
+        clocks = ClockSampler(dev)
+        clocks.start()  # sampling spans warm-up + timed steps (nvidia-smi needs ~0.5 s to start)
         for _ in range(args.warmup):
             step()
         ctx.synchronize()
-        clocks = ClockSampler(dev)
-        clocks.start()
         launches0 = ctx.launches()
         ctx.profile_begin()
         ctx.record(0)
@@ -237,7 +237,6 @@ def run_single(args) -> None:
         dev_ms = ctx.elapsed_ms(0, 1)
         profile = ctx.profile_end()
         launches = ctx.launches() - launches0
-        clk = clocks.stop()
         stages = ctx.stage_times()
         rounds = ctx.sa_rounds()
         T = int(total[0])
@@ -248,6 +247,7 @@ def run_single(args) -> None:
             step()
         ctx.record(1)
         dev_ms_plain = ctx.elapsed_ms(0, 1)
+        clk = clocks.stop()
     ms_per_step = min(dev_ms, dev_ms_plain) / args.steps
     value = n / (ms_per_step * 1e-3)
 
@@ -306,7 +306,7 @@ def run_single(args) -> None:
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="C3")

@@ -140,17 +140,26 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
         sm.tile_start[d] = excl;
         u64 prefix = 0;
         if (tile > 0) {
+            // look back 4 predecessor tiles per step (4 loads in flight)
             long long t = tile - 1;
             while (true) {
-                u64 s;
-                s = ld_relaxed(status + (size_t)t * kRadix + d);
-                while ((s >> 62) == 0) {
-                    __nanosleep(20);
-                    s = ld_relaxed(status + (size_t)t * kRadix + d);
+                u64 s[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    s[q] = (t - q >= 0) ? ld_relaxed(status + (size_t)(t - q) * kRadix + d) : kFlagPre;
+                bool done = false;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (done) break;
+                    while ((s[q] >> 62) == 0) {
+                        __nanosleep(20);
+                        s[q] = ld_relaxed(status + (size_t)(t - q) * kRadix + d);
+                    }
+                    prefix += s[q] & kValMask;
+                    if ((s[q] >> 62) == 2) done = true;
                 }
-                prefix += s & kValMask;
-                if ((s >> 62) == 2) break;
-                --t;
+                if (done) break;
+                t -= 4;
             }
             st_relaxed(status + (size_t)tile * kRadix + d, kFlagPre | (prefix + run));
         }
