@@ -118,6 +118,133 @@ __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict
     bounds[2 * g + 1] = hi;
 }
 
+struct TileCtx {
+    long long tile, cnt, tile_k0, tile_k1, slot0, tiles, flat_cap;
+    int npos, out_off;
+    unsigned *s_lo, *s_hi, *s_cnt, *s_warp;
+    u64 *s_base;
+    long long *out0, *out1, *flat;
+    u64 *status;
+    unsigned long long *total_out;
+};
+
+// Everything after staging.  Inlined twice (candidates in shared memory or,
+// for oversized windows, in global memory) so each copy uses the right
+// address space (LDS instead of generic loads).
+template <bool RAW, bool ALL>
+__device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x) {
+    const long long cnt = x.cnt, tile_k0 = x.tile_k0, tile_k1 = x.tile_k1;
+    for (long long t = threadIdx.x; t < cnt; t += kNT) {
+        long long ep = t ? c.end(t - 1) : tile_k0 - 1;
+        long long a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
+        long long b = c.end(t);
+        if (b > tile_k1) b = tile_k1;
+        for (long long k = a; k <= b; ++k) x.s_lo[k - tile_k0] = (unsigned)t;
+        long long sn = (t + 1 < cnt) ? c.start(t + 1) : tile_k1 + 1;
+        a = c.start(t) > tile_k0 ? c.start(t) : tile_k0;
+        b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
+        for (long long k = a; k <= b; ++k) x.s_hi[k - tile_k0] = (unsigned)(t + 1);
+    }
+    __syncthreads();
+
+    // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
+    unsigned best[kPPT];
+    unsigned first[kPPT];  // start of the first tie (positions with one tie skip the re-walk)
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x + j * kNT;
+        best[j] = 0;
+        first[j] = 0;
+        if (p >= x.npos) continue;
+        const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
+        unsigned bl = 0, nt = 0;
+        long long bs = -1;
+        for (unsigned t = wl; t < wh; ++t) {
+            const unsigned L = c.len(t);
+            if (L > bl) {
+                bl = L;
+                bs = c.start(t);
+                nt = 1;
+            } else if (L == bl) {
+                ++nt;
+            }
+        }
+        best[j] = bl;
+        first[j] = (unsigned)bs;
+        if (ALL) {
+            x.out0[x.slot0 + p] = bl;
+            x.s_cnt[p] = bl ? nt : 0;
+        } else {
+            x.out0[x.slot0 + p] = bl ? bs : -1;
+            x.out1[x.slot0 + p] = bl;
+        }
+    }
+    if (!ALL) {
+        if (x.tile == 0 && threadIdx.x == 0 && x.out_off) {
+            x.out0[0] = -1;
+            x.out1[0] = 0;
+        }
+        return;
+    }
+
+    // ---- all ties: exclusive scan of the tile's counts (position order) ----
+    __syncthreads();
+    unsigned mine[kPPT], msum = 0;
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x * kPPT + j;
+        mine[j] = p < x.npos ? x.s_cnt[p] : 0;
+        msum += mine[j];
+    }
+    unsigned excl;
+    const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, x.s_warp);
+    if (threadIdx.x < 32) {
+        u64 base = lookback_warp(x.status, x.tile, (u64)block_total, OpSum());
+        if (threadIdx.x == 0) {
+            *x.s_base = base;
+            if (x.tile == x.tiles - 1) *x.total_out = base + block_total;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x * kPPT + j;
+        if (p < x.npos) x.s_cnt[p] = excl;
+        excl += mine[j];
+    }
+    __syncthreads();
+    const u64 tile_base = *x.s_base;
+    if (x.tile == 0 && threadIdx.x == 0) {
+        if (x.out_off) {
+            x.out0[0] = 0;  // lengths[0]
+            x.out1[0] = 0;  // offsets[0]
+        }
+        x.out1[x.out_off] = 0;  // offsets of the first position
+    }
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x + j * kNT;
+        if (p >= x.npos) continue;
+        const unsigned ex = x.s_cnt[p];
+        const unsigned nxt = (p + 1 < x.npos) ? x.s_cnt[p + 1] : block_total;
+        x.out1[x.slot0 + 1 + p] = (long long)(tile_base + nxt);  // offsets[k+1] = inclusive prefix
+        const unsigned nt = nxt - ex;
+        if (nt == 0) continue;
+        long long w = (long long)(tile_base + ex);
+        if (nt == 1) {
+            if (w < x.flat_cap) x.flat[w] = first[j];
+            continue;
+        }
+        const unsigned bl = best[j];
+        const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
+        for (unsigned t = wl; t < wh; ++t) {
+            if (c.len(t) == bl) {
+                if (w < x.flat_cap) x.flat[w] = c.start(t);
+                ++w;
+            }
+        }
+    }
+}
+
 // Query kernel.  out_off = 1 writes the reference 1-based padded layout
 // (slot k), out_off = 0 writes a shard-local layout (slot k - kb).
 template <bool RAW, bool ALL>
@@ -129,9 +256,6 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
                                                long long tiles, unsigned long long *total_out) {
     extern __shared__ __align__(128) unsigned char dsm[];
     unsigned char *s_stage = dsm;
-    unsigned *s_lo = reinterpret_cast<unsigned *>(dsm + kStageBytes);  // window start per position
-    unsigned *s_hi = s_lo + kG;                                         // window end (exclusive)
-    unsigned *s_cnt = s_hi + kG;                                        // tie counts -> exclusive offsets
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ unsigned s_tile;
     __shared__ unsigned s_warp[kNT / 32];
@@ -145,150 +269,60 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     } else {
         tile = blockIdx.x;
     }
+    TileCtx x;
+    x.tile = tile;
     const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];
-    const long long cnt = hi - lo;
-    const long long tile_k0 = kb + tile * kG;
-    const int npos = (int)((ke - tile_k0 + 1) < kG ? (ke - tile_k0 + 1) : kG);
-    const long long tile_k1 = tile_k0 + npos - 1;  // last position of the tile
+    x.cnt = hi - lo;
+    x.tile_k0 = kb + tile * kG;
+    x.npos = (int)((ke - x.tile_k0 + 1) < kG ? (ke - x.tile_k0 + 1) : kG);
+    x.tile_k1 = x.tile_k0 + x.npos - 1;
+    x.slot0 = x.tile_k0 - kb + out_off;
+    x.out_off = out_off;
+    x.tiles = tiles;
+    x.flat_cap = flat_cap;
+    x.s_lo = reinterpret_cast<unsigned *>(dsm + kStageBytes);  // window start per position
+    x.s_hi = x.s_lo + kG;                                       // window end (exclusive)
+    x.s_cnt = x.s_hi + kG;                                      // tie counts -> exclusive offsets
+    x.s_warp = s_warp;
+    x.s_base = &s_base;
+    x.out0 = out0;
+    x.out1 = out1;
+    x.flat = flat;
+    x.status = status;
+    x.total_out = total_out;
 
     // ---- stage the tile's candidate range [lo, hi) with one TMA bulk copy ----
+    const int esz = RAW ? 4 : 8;
+    const long long align = 16 / esz;
+    const long long a = lo & ~(align - 1), b = (hi + align - 1) & ~(align - 1);
+    const bool fits = x.cnt > 0 && b - a <= (RAW ? kCapR : kCapC);
+    if (fits && threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        unsigned bytes = (unsigned)((b - a) * esz);
+        mbar_expect_tx(&s_bar, bytes);
+        tma_load_1d(s_stage, RAW ? (const void *)(raw + a) : (const void *)(e + a), bytes, &s_bar);
+    }
+    // window bounds per position: every position's window is the contiguous
+    // candidate range [lo(k), hi(k)); lo(k) = first candidate with end >= k,
+    // hi(k) = #candidates with start <= k.  Both are nondecreasing, so each
+    // candidate fills the positions where it is the boundary -- O(tile +
+    // candidates), no searches.
+    for (int i = threadIdx.x; i < x.npos; i += kNT) {
+        x.s_lo[i] = (unsigned)x.cnt;
+        x.s_hi[i] = 0;
+    }
+    __syncthreads();
     Cand<RAW> c;
-    c.e = nullptr;
-    c.r = nullptr;
     c.base = lo;
-    {
-        const int esz = RAW ? 4 : 8;
-        const long long align = 16 / esz;
-        long long a = lo & ~(align - 1), b = (hi + align - 1) & ~(align - 1);
-        const bool fits = cnt > 0 && b - a <= (RAW ? kCapR : kCapC);
-        if (fits) {
-            if (threadIdx.x == 0) {
-                mbar_init(&s_bar, 1);
-                unsigned bytes = (unsigned)((b - a) * esz);
-                mbar_expect_tx(&s_bar, bytes);
-                tma_load_1d(s_stage, RAW ? (const void *)(raw + a) : (const void *)(e + a), bytes, &s_bar);
-            }
-        }
-        // window bounds per position: every position's window is the
-        // contiguous candidate range [lo(k), hi(k)); lo(k) = first candidate
-        // with end >= k, hi(k) = #candidates with start <= k.  Both are
-        // nondecreasing, so each candidate fills the positions where it is
-        // the boundary -- O(tile + candidates), no searches.
-        for (int i = threadIdx.x; i < npos; i += kNT) {
-            s_lo[i] = (unsigned)cnt;
-            s_hi[i] = 0;
-        }
-        __syncthreads();
-        if (fits) {
-            mbar_wait(&s_bar, 0);
-            if (RAW) c.r = reinterpret_cast<const unsigned *>(s_stage) + (lo - a);
-            else c.e = reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
-        } else {
-            if (RAW) c.r = raw + lo;
-            else c.e = e + lo;
-        }
-    }
-    for (long long t = threadIdx.x; t < cnt; t += kNT) {
-        long long ep = t ? c.end(t - 1) : tile_k0 - 1;
-        long long a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
-        long long b = c.end(t);
-        if (b > tile_k1) b = tile_k1;
-        for (long long k = a; k <= b; ++k) s_lo[k - tile_k0] = (unsigned)t;
-        long long sn = (t + 1 < cnt) ? c.start(t + 1) : tile_k1 + 1;
-        a = c.start(t) > tile_k0 ? c.start(t) : tile_k0;
-        b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
-        for (long long k = a; k <= b; ++k) s_hi[k - tile_k0] = (unsigned)(t + 1);
-    }
-    __syncthreads();
-
-    // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
-    const long long slot0 = tile_k0 - kb + out_off;
-    unsigned best[kPPT];
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x + j * kNT;
-        best[j] = 0;
-        if (p >= npos) continue;
-        const unsigned wl = s_lo[p], wh = s_hi[p];
-        unsigned bl = 0, nt = 0;
-        long long bs = -1;
-        for (unsigned t = wl; t < wh; ++t) {
-            unsigned L = c.len(t);
-            if (L > bl) {
-                bl = L;
-                bs = c.start(t);
-                nt = 1;
-            } else if (L == bl) {
-                ++nt;
-            }
-        }
-        best[j] = bl;
-        if (ALL) {
-            out0[slot0 + p] = bl;
-            s_cnt[p] = bl ? nt : 0;
-        } else {
-            out0[slot0 + p] = bl ? bs : -1;
-            out1[slot0 + p] = bl;
-        }
-    }
-    if (!ALL) {
-        if (tile == 0 && threadIdx.x == 0 && out_off) {
-            out0[0] = -1;
-            out1[0] = 0;
-        }
-        return;
-    }
-
-    // ---- all ties: exclusive scan of the tile's counts (position order) ----
-    __syncthreads();
-    unsigned mine[kPPT], msum = 0;
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x * kPPT + j;
-        mine[j] = p < npos ? s_cnt[p] : 0;
-        msum += mine[j];
-    }
-    unsigned excl;
-    const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, s_warp);
-    if (threadIdx.x < 32) {
-        u64 base = lookback_warp(status, tile, (u64)block_total, OpSum());
-        if (threadIdx.x == 0) {
-            s_base = base;
-            if (tile == tiles - 1) *total_out = base + block_total;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x * kPPT + j;
-        if (p < npos) s_cnt[p] = excl;
-        excl += mine[j];
-    }
-    __syncthreads();
-    const u64 tile_base = s_base;
-    if (tile == 0 && threadIdx.x == 0) {
-        if (out_off) {
-            out0[0] = 0;  // lengths[0]
-            out1[0] = 0;  // offsets[0]
-        }
-        out1[out_off] = 0;  // offsets of the first position
-    }
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x + j * kNT;
-        if (p >= npos) continue;
-        const unsigned ex = s_cnt[p];
-        const unsigned nxt = (p + 1 < npos) ? s_cnt[p + 1] : block_total;
-        out1[slot0 + 1 + p] = (long long)(tile_base + nxt);  // offsets[k+1] = inclusive prefix
-        const unsigned bl = best[j];
-        if (nxt == ex) continue;
-        u64 w = tile_base + ex;
-        const unsigned wl = s_lo[p], wh = s_hi[p];
-        for (unsigned t = wl; t < wh; ++t) {
-            if (c.len(t) == bl) {
-                if ((long long)w < flat_cap) flat[w] = c.start(t);
-                ++w;
-            }
-        }
+    if (fits) {
+        mbar_wait(&s_bar, 0);
+        c.e = RAW ? nullptr : reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
+        c.r = RAW ? reinterpret_cast<const unsigned *>(s_stage) + (lo - a) : nullptr;
+        query_tile<RAW, ALL>(c, x);
+    } else {
+        c.e = RAW ? nullptr : e + lo;
+        c.r = RAW ? raw + lo : nullptr;
+        query_tile<RAW, ALL>(c, x);
     }
 }
 
