@@ -65,15 +65,18 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
 }
 
 // Candidate window view: compact entries (start, len) or raw values (start = base + t).
+// Positions are < 2^31, so candidate starts/ends are 32-bit.
 template <bool RAW>
 struct Cand {
     const uint2 *e;       // compact
     const unsigned *r;    // raw
-    long long base;       // raw: text index of r[0]
-    __device__ __forceinline__ long long start(long long t) const { return RAW ? base + t : (long long)e[t].x; }
-    __device__ __forceinline__ unsigned len(long long t) const { return RAW ? r[t] : e[t].y; }
-    __device__ __forceinline__ long long end(long long t) const {
-        return RAW ? base + t + (long long)r[t] - 1 : (long long)e[t].x + (long long)e[t].y - 1;
+    unsigned base;        // raw: text index of r[0]
+    __device__ __forceinline__ unsigned start(unsigned t) const { return RAW ? base + t : e[t].x; }
+    __device__ __forceinline__ unsigned len(unsigned t) const { return RAW ? r[t] : e[t].y; }
+    __device__ __forceinline__ int end(unsigned t) const {
+        if (RAW) return (int)(base + t + r[t]) - 1;
+        const uint2 v = e[t];
+        return (int)(v.x + v.y) - 1;
     }
 };
 
@@ -133,17 +136,19 @@ struct TileCtx {
 // address space (LDS instead of generic loads).
 template <bool RAW, bool ALL>
 __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x) {
-    const long long cnt = x.cnt, tile_k0 = x.tile_k0, tile_k1 = x.tile_k1;
-    for (long long t = threadIdx.x; t < cnt; t += kNT) {
-        long long ep = t ? c.end(t - 1) : tile_k0 - 1;
-        long long a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
-        long long b = c.end(t);
-        if (b > tile_k1) b = tile_k1;
-        for (long long k = a; k <= b; ++k) x.s_lo[k - tile_k0] = (unsigned)t;
-        long long sn = (t + 1 < cnt) ? c.start(t + 1) : tile_k1 + 1;
-        a = c.start(t) > tile_k0 ? c.start(t) : tile_k0;
+    const unsigned cnt = (unsigned)x.cnt;
+    const int tile_k0 = (int)x.tile_k0, tile_k1 = (int)x.tile_k1;
+    for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
+        const int ep = t ? c.end(t - 1) : tile_k0 - 1;
+        const int e_t = c.end(t);
+        int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
+        int b = e_t < tile_k1 ? e_t : tile_k1;
+        for (int k = a; k <= b; ++k) x.s_lo[k - tile_k0] = t;
+        const int st = (int)c.start(t);
+        const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
+        a = st > tile_k0 ? st : tile_k0;
         b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
-        for (long long k = a; k <= b; ++k) x.s_hi[k - tile_k0] = (unsigned)(t + 1);
+        for (int k = a; k <= b; ++k) x.s_hi[k - tile_k0] = t + 1;
     }
     __syncthreads();
 
@@ -157,8 +162,7 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         first[j] = 0;
         if (p >= x.npos) continue;
         const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
-        unsigned bl = 0, nt = 0;
-        long long bs = -1;
+        unsigned bl = 0, nt = 0, bs = 0;
         for (unsigned t = wl; t < wh; ++t) {
             const unsigned L = c.len(t);
             if (L > bl) {
@@ -170,12 +174,12 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
             }
         }
         best[j] = bl;
-        first[j] = (unsigned)bs;
+        first[j] = bs;
         if (ALL) {
             x.out0[x.slot0 + p] = bl;
             x.s_cnt[p] = bl ? nt : 0;
         } else {
-            x.out0[x.slot0 + p] = bl ? bs : -1;
+            x.out0[x.slot0 + p] = bl ? (long long)bs : -1ll;
             x.out1[x.slot0 + p] = bl;
         }
     }
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     }
     __syncthreads();
     Cand<RAW> c;
-    c.base = lo;
+    c.base = (unsigned)lo;
     if (fits) {
         mbar_wait(&s_bar, 0);
         c.e = RAW ? nullptr : reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
