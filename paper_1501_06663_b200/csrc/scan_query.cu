@@ -143,11 +143,13 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         const int e_t = c.end(t);
         int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
         int b = e_t < tile_k1 ? e_t : tile_k1;
+#pragma unroll 1
         for (int k = a; k <= b; ++k) x.s_lo[k - tile_k0] = t;
         const int st = (int)c.start(t);
         const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
         a = st > tile_k0 ? st : tile_k0;
         b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
+#pragma unroll 1
         for (int k = a; k <= b; ++k) x.s_hi[k - tile_k0] = t + 1;
     }
     __syncthreads();
@@ -163,6 +165,7 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         if (p >= x.npos) continue;
         const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
         unsigned bl = 0, nt = 0, bs = 0;
+#pragma unroll 1
         for (unsigned t = wl; t < wh; ++t) {
             const unsigned L = c.len(t);
             if (L > bl) {
@@ -240,6 +243,7 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         }
         const unsigned bl = best[j];
         const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
+#pragma unroll 1
         for (unsigned t = wl; t < wh; ++t) {
             if (c.len(t) == bl) {
                 if (w < x.flat_cap) x.flat[w] = c.start(t);
