@@ -5,9 +5,11 @@
 //
 // B200 design (prefix doubling with group-head ranks, Larsson-Sadakane style):
 //   round 0: every suffix gets a packed key of its first K symbols, each an
-//            order-preserving code 1..sigma (0 = past the end) of b bits.
+//            order-preserving code 0..sigma-1 of b = ceil(log2 sigma) bits
+//            (2 bits for DNA); past the end pads with code 0, and the ties
+//            that creates are broken by suffix length in the next round.
 //            K is the largest count that fits the fewest 8-bit radix passes
-//            while sigma^K >= 16 n (DNA at 256 Mi: b = 3, K = 16, 6 passes).
+//            while sigma^K >= 16 n (DNA at 256 Mi: b = 2, K = 16, 4 passes).
 //            One LSD radix sort of (key, position) pairs gives the SA order.
 //   k_update: SA write-back, ISA = SA slot of the suffix's group head
 //            (max-scan) and compaction of the still-unsorted slots (sum-scan),
@@ -80,8 +82,14 @@ __global__ void __launch_bounds__(256) k_init_keys(const unsigned char *__restri
     if (i >= n) return;
     u64 key = 0;
     for (int j = 0; j < K; ++j) key = (key << b) | s[threadIdx.x + j];
-    keys[i] = key;
-    vals[i] = (unsigned)i;
+    // Input order of the stable sort: the S = min(K-1, n) short suffixes
+    // (fewer than K symbols, padded) first by increasing length, then the rest
+    // by position -- so among equal padded keys a short suffix (a proper
+    // prefix of the others) precedes them, as the true order requires.
+    const long long S = (long long)K - 1 < n ? (long long)K - 1 : n;
+    const long long e = (n - i < K) ? n - 1 - i : i + S;
+    keys[e] = key;
+    vals[e] = (unsigned)i;
 }
 
 // Round r >= 1 keys for the unsorted slots P[0..U).
@@ -92,8 +100,11 @@ __global__ void k_make_keys(const unsigned *__restrict__ P, long long U, const u
     if (t >= U) return;
     unsigned i = sa[P[t]];
     u64 hi = isa[i];
-    u64 lo = ((long long)i + h < n) ? (u64)isa[i + h] + 1 : 0;
-    keys[t] = hi * (u64)(n + 1) + lo;
+    // Suffixes shorter than h (padded with the smallest code) order by length
+    // before every longer member of their group: lo = remaining length in
+    // [1, h]; otherwise h + 1 + rank of suffix i + h.
+    u64 lo = ((long long)i + h < n) ? (u64)(h + 1) + isa[i + h] : (u64)(n - i);
+    keys[t] = hi * (u64)(n + h + 1) + lo;
     vals[t] = i;
 }
 
@@ -101,9 +112,18 @@ constexpr int kUNT = 256;
 constexpr int kUIPT = 8;
 constexpr int kUTile = kUNT * kUIPT;
 
-__device__ __forceinline__ unsigned key_lcp(u64 a, u64 b, int code_bits, int key_bits) {
-    u64 x = a ^ b;
-    return x ? (unsigned)((__clzll((long long)x) - (64 - key_bits)) / code_bits) : kLcpUnknown;
+// LCP of two suffixes from their packed K-symbol keys (codes 0..sigma-1, the
+// smallest code also pads past the end), capped by their remaining lengths.
+// Equal keys with both suffixes >= K long: unknown (>= K), fixed later.
+__device__ __forceinline__ unsigned key_lcp(u64 a, u64 b, int code_bits, int key_bits, unsigned K,
+                                            unsigned rem_a, unsigned rem_b) {
+    const u64 x = a ^ b;
+    const unsigned m = rem_a < rem_b ? rem_a : rem_b;
+    if (x) {
+        const unsigned l = (unsigned)((__clzll((long long)x) - (64 - key_bits)) / code_bits);
+        return l < m ? l : m;
+    }
+    return m < K ? m : kLcpUnknown;
 }
 
 // Write back one sorted run of (key, suffix) pairs occupying SA slots Pos(t)
@@ -146,13 +166,31 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
     u64 knext = __shfl_down_sync(0xffffffffu, k[0], 1);
     if (lane == 0) kprev = (t0 > 0 && t0 - 1 < U) ? keys[t0 - 1] : 0;
     if (lane == 31) knext = (t0 + kUIPT < U) ? keys[t0 + kUIPT] : 0;
+    // round 0: a short suffix (fewer than K symbols) is never tied -- its
+    // padded key may equal longer suffixes' keys, but the input order already
+    // placed it correctly (k_init_keys), so it forms its own group.
+    bool shortf[kUIPT + 2];  // shortness of items j-1 .. j+... (index j+1)
+    if (!P) {
+        const unsigned Ks = (unsigned)(key_bits / code_bits);
+#pragma unroll
+        for (int j = 0; j < kUIPT; ++j) {
+            const long long t = t0 + j;
+            shortf[j + 1] = t < U && (unsigned)(U - vals[t]) < Ks;
+        }
+        const long long tp = t0 - 1, tn = t0 + kUIPT;
+        shortf[0] = tp >= 0 && (unsigned)(U - vals[tp]) < Ks;
+        shortf[kUIPT + 1] = tn < U && (unsigned)(U - vals[tn]) < Ks;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kUIPT + 2; ++j) shortf[j] = false;
+    }
     bool newf[kUIPT + 1];
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) {
         long long t = t0 + j;
-        newf[j] = (t == 0) || (k[j] != (j ? k[j - 1] : kprev));
+        newf[j] = (t == 0) || (k[j] != (j ? k[j - 1] : kprev)) || shortf[j] || shortf[j + 1];
     }
-    newf[kUIPT] = (t0 + kUIPT >= U) || (knext != k[kUIPT - 1]);
+    newf[kUIPT] = (t0 + kUIPT >= U) || (knext != k[kUIPT - 1]) || shortf[kUIPT] || shortf[kUIPT + 1];
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j)
         if (t0 + j + 1 == U) newf[j + 1] = true;
@@ -220,16 +258,26 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
     __syncthreads();
     for (int i = threadIdx.x; i < tile_n; i += kUNT) sa[tile_t0 + i] = s_stage[i];
     __syncthreads();
-    // LCP of adjacent suffixes from their packed K-symbol keys when they
-    // differ; kLcpUnknown (true LCP >= K) otherwise.
+    // LCP of adjacent suffixes from their packed K-symbol keys (capped by the
+    // suffix lengths); kLcpUnknown (true LCP >= K) when undecided.
+    const unsigned K = (unsigned)(key_bits / code_bits);
+    unsigned vprev = __shfl_up_sync(0xffffffffu, vv[kUIPT - 1], 1);
+    unsigned vnext = __shfl_down_sync(0xffffffffu, vv[0], 1);
+    if (lane == 0) vprev = t0 > 0 ? vals[t0 - 1] : 0;
+    if (lane == 31) vnext = (t0 + kUIPT < U) ? vals[t0 + kUIPT] : 0;
+    const unsigned nn = (unsigned)U;  // round 0: U == n
     unsigned lk[kUIPT + 1];
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) {
         long long t = t0 + j;
-        lk[j] = (t > 0 && t < U) ? key_lcp(k[j], j ? k[j - 1] : kprev, code_bits, key_bits) : 0;
+        const unsigned vp = j ? vv[j - 1] : vprev;
+        lk[j] = (t > 0 && t < U) ? key_lcp(k[j], j ? k[j - 1] : kprev, code_bits, key_bits, K, nn - vv[j], nn - vp)
+                                 : 0;
         s_stage[threadIdx.x * kUIPT + j] = lk[j];
     }
-    lk[kUIPT] = (t0 + kUIPT < U) ? key_lcp(knext, k[kUIPT - 1], code_bits, key_bits) : 0;
+    lk[kUIPT] = (t0 + kUIPT < U)
+                    ? key_lcp(knext, k[kUIPT - 1], code_bits, key_bits, K, nn - vnext, nn - vv[kUIPT - 1])
+                    : 0;
     __syncthreads();
     for (int i = threadIdx.x; i < tile_n; i += kUNT) lcp_d[tile_t0 + i] = s_stage[i];
     // raw LLR candidate of each suffix: max(LCP with SA predecessor, with
@@ -392,9 +440,11 @@ void build_suffix_array(rs_ctx *c, long long n) {
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * 256);
     CodeTable ct;
     int sigma = 0;
-    for (int b = 0; b < 256; ++b) ct.code[b] = h[b] ? (unsigned short)(++sigma) : 0;
+    // order-preserving codes 0..sigma-1; past the end pads with code 0 too
+    // (ties this creates are broken by suffix length in the next rounds)
+    for (int b = 0; b < 256; ++b) ct.code[b] = h[b] ? (unsigned short)(sigma++) : 0;
     int bits = 1;
-    while ((1 << bits) < sigma + 1) ++bits;
+    while ((1 << bits) < sigma) ++bits;
     // Round-0 key length: all Kmax symbols that fit in 64 bits, unless fewer
     // already separate i.i.d. text (sigma^K >= 16 n) with fewer 8-bit radix
     // passes; the prefix-doubling rounds resolve whatever stays tied.
@@ -431,8 +481,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
     const unsigned *P = nullptr;
     long long depth = K;
     // bits of a round key hi*(n+1)+lo < n*(n+1)
-    int rbits = (int)std::ceil(std::log2((double)n * (double)(n + 1)));
-    if (rbits < 1) rbits = 1;
+
     while (true) {
         ++c->sa_rounds;
         long long tiles = (U + kUTile - 1) / kUTile;
@@ -458,6 +507,9 @@ void build_suffix_array(rs_ctx *c, long long n) {
         std::swap(Pa, Pb);  // Pb now holds the unsorted list
         P = Pb;
         RS_LAUNCH_B(c, 28.0 * U, k_make_keys, grid_for(U, 256), 256, 0, P, U, sa, isa, n, depth, k0, v0);
+        // bits of a round key hi*(n+h+1)+lo < n*(n+h+1)
+        int rbits = (int)std::ceil(std::log2((double)n * (double)(n + depth + 1)));
+        if (rbits < 1) rbits = 1;
         radix_sort_pairs(c, k0, k1, v0, v1, U, rbits, &ks, &vs);
         depth *= 2;
     }
