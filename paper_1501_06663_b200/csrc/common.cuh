@@ -62,6 +62,7 @@ enum BufId {
     B_T4,
     B_T5,
     B_PATCH,     // list of patched LCP slots
+    B_PACKED,    // text packed as b-bit codes
     B_COUNT
 };
 
@@ -340,7 +341,31 @@ void build_lcp(rs_ctx *c, long long n);                  // B_TEXT, B_SA, B_ISA 
 // radix_sort.cu
 // Sorts (keys, vals) pairs by the low `bits` bits of keys, stable.  Result
 // lands in the returned buffers (ping-pong between the two given pairs).
+// Round-0 keys generated on the fly from the text packed as a big-endian bit
+// stream of b-bit symbol codes: key(p) = bits [b*p, b*p + b*K) of the stream,
+// and the element order is the suffix-sort input order (short suffixes first).
+struct TextKeys {
+    const u64 *stream;   // packed codes, zero padded past the end
+    long long n;         // text length
+    int b, K;            // code bits, symbols per key
+    long long S;         // number of short suffixes placed first
+};
+__device__ __forceinline__ u64 text_key(const TextKeys &tk, long long p) {
+    const long long o = (long long)tk.b * p;
+    const u64 *w = tk.stream + (o >> 6);
+    const unsigned sh = (unsigned)(o & 63);
+    u64 x = w[0];
+    if (sh) x = (x << sh) | (w[1] >> (64 - sh));
+    const int kb = tk.b * tk.K;
+    return kb >= 64 ? x : (x >> (64 - kb));
+}
+__device__ __forceinline__ long long text_pos(const TextKeys &tk, long long e) {
+    return e < tk.S ? tk.n - 1 - e : e - tk.S;
+}
+// Sorts (keys, vals) pairs by the low `bits` bits of keys, stable.  With tk,
+// the input pairs are generated from the packed text (keys/vals unread).
 void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsigned *vals_alt,
-                      long long count, int bits, u64 **keys_out, unsigned **vals_out);
+                      long long count, int bits, u64 **keys_out, unsigned **vals_out,
+                      const TextKeys *tk = nullptr);
 
 }  // namespace rsb

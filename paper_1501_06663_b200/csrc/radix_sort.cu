@@ -24,14 +24,16 @@ constexpr int kTile = kNT * kIPT;  // 3072 pairs per tile
 constexpr int kWarps = kNT / 32;
 constexpr int kRadix = 256;
 
+template <bool TEXT>
 __global__ void __launch_bounds__(kNT) k_histograms(const u64 *__restrict__ keys, long long count, int passes,
-                                                    unsigned long long *__restrict__ hist /*[passes][256]*/) {
+                                                    unsigned long long *__restrict__ hist /*[passes][256]*/,
+                                                    TextKeys tk) {
     __shared__ unsigned s_hist[8][kRadix];
     for (int i = threadIdx.x; i < 8 * kRadix; i += kNT) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     long long stride = (long long)gridDim.x * kNT;
     for (long long i = blockIdx.x * (long long)kNT + threadIdx.x; i < count; i += stride) {
-        u64 k = keys[i];
+        u64 k = TEXT ? text_key(tk, i) : keys[i];  // histograms need no particular order
         for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
     }
     __syncthreads();
@@ -56,6 +58,15 @@ __global__ void k_hist_scan(unsigned long long *hist) {
     h[threadIdx.x] = s[threadIdx.x] - h[threadIdx.x];
 }
 
+// (key, suffix) pairs straight from the packed text, in sort input order.
+__global__ void k_materialize(TextKeys tk, long long count, u64 *__restrict__ keys, unsigned *__restrict__ vals) {
+    long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    const long long pos = text_pos(tk, e);
+    keys[e] = text_key(tk, pos);
+    vals[e] = (unsigned)pos;
+}
+
 struct SortSmem {
     u64 keys[kTile];
     unsigned vals[kTile];
@@ -66,11 +77,12 @@ struct SortSmem {
     unsigned tile_id;
 };
 
+template <bool TEXT>
 __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
                                                   u64 *__restrict__ keys_out, unsigned *__restrict__ vals_out,
                                                   long long count, int shift,
                                                   const unsigned long long *__restrict__ digit_base,
-                                                  unsigned *counter, u64 *status /*[tiles][256]*/) {
+                                                  unsigned *counter, u64 *status /*[tiles][256]*/, TextKeys tk) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -88,8 +100,14 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
     for (int i = 0; i < kIPT; ++i) {
         long long idx = base + i * 32 + lane;
         if (idx < count) {
-            k[i] = keys_in[idx];
-            v[i] = vals_in[idx];
+            if (TEXT) {  // first pass of the round-0 sort: pairs straight from the packed text
+                const long long pos = text_pos(tk, idx);
+                k[i] = text_key(tk, pos);
+                v[i] = (unsigned)pos;
+            } else {
+                k[i] = keys_in[idx];
+                v[i] = vals_in[idx];
+            }
         }
     }
     // 1) tile digit histogram first, published right away (decoupled
@@ -192,16 +210,23 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
 }  // namespace
 
 void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsigned *vals_alt,
-                      long long count, int bits, u64 **keys_out, unsigned **vals_out) {
+                      long long count, int bits, u64 **keys_out, unsigned **vals_out, const TextKeys *tk) {
+    const TextKeys tkv = tk ? *tk : TextKeys{nullptr, 0, 0, 0, 0};
     *keys_out = keys;
     *vals_out = vals;
-    if (count <= 1 || bits <= 0) return;
+    if (count <= 1 || bits <= 0) {
+        if (tk && count > 0) RS_LAUNCH(c, k_materialize, grid_for(count, 256), 256, 0, tkv, count, keys, vals);
+        return;
+    }
     int passes = (bits + 7) / 8;
     if (passes > 8) passes = 8;
     unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * kRadix);
     RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
     unsigned hist_blocks = (unsigned)std::min<long long>((count + kNT * 16 - 1) / (kNT * 16), c->sm_count * 8);
-    RS_LAUNCH_B(c, 8.0 * count, k_histograms, hist_blocks, kNT, 0, keys, count, passes, hist);
+    if (tk)
+        RS_LAUNCH_B(c, 0.25 * count, k_histograms<true>, hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+    else
+        RS_LAUNCH_B(c, 8.0 * count, k_histograms<false>, hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
     // Host needs the histograms to skip constant-digit passes.
     std::vector<unsigned long long> h((size_t)passes * kRadix);
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
@@ -209,21 +234,29 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
 
     static bool attr_set = false;
     if (!attr_set) {
-        RS_CUDA(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RS_CUDA(cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(SortSmem)));
+        RS_CUDA(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(SortSmem)));
         attr_set = true;
     }
     long long tiles = (count + kTile - 1) / kTile;
     u64 *kin = keys, *kout = keys_alt;
     unsigned *vin = vals, *vout = vals_alt;
+    bool from_text = tk != nullptr;
     for (int p = 0; p < passes; ++p) {
         bool trivial = false;
         for (int d = 0; d < kRadix; ++d)
             if (h[(size_t)p * kRadix + d] == (unsigned long long)count) trivial = true;
-        if (trivial) continue;
+        if (trivial && !(from_text && p == passes - 1)) continue;  // the text must be materialised once
         Scratch s = scratch(c, tiles * kRadix);
-        RS_LAUNCH_B(c, 24.0 * count, k_onesweep, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout, vout, count, 8 * p,
-                  hist + (size_t)p * kRadix, s.counter, s.status);
+        if (from_text)
+            RS_LAUNCH_B(c, 12.25 * count, k_onesweep<true>, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout,
+                        vout, count, 8 * p, hist + (size_t)p * kRadix, s.counter, s.status, tkv);
+        else
+            RS_LAUNCH_B(c, 24.0 * count, k_onesweep<false>, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout,
+                        vout, count, 8 * p, hist + (size_t)p * kRadix, s.counter, s.status, tkv);
+        from_text = false;
         std::swap(kin, kout);
         std::swap(vin, vout);
     }

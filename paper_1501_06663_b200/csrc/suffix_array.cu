@@ -67,29 +67,23 @@ __global__ void k_byte_hist(const unsigned char *__restrict__ text, long long n,
     if (s[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)s[threadIdx.x]);
 }
 
-// key[i] = sum_j code(text[i+j]) << (b*(K-1-j)), j < K, code 0 past the end.
-__global__ void __launch_bounds__(256) k_init_keys(const unsigned char *__restrict__ text, long long n, CodeTable ct,
-                                                   int b, int K, u64 *__restrict__ keys,
-                                                   unsigned *__restrict__ vals) {
-    __shared__ unsigned short s[256 + 64];
-    long long base = blockIdx.x * 256ll;
-    for (int j = threadIdx.x; j < 256 + K; j += 256) {
-        long long p = base + j;
-        s[j] = p < n ? ct.code[text[p]] : 0;
+// Text -> big-endian bit stream of b-bit codes (one 64-bit word per thread),
+// zero padded past the end.
+__global__ void k_pack_text(const unsigned char *__restrict__ text, long long n, CodeTable ct, int b,
+                            long long words, u64 *__restrict__ stream) {
+    long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (w >= words) return;
+    const long long bit0 = w * 64;
+    long long p = bit0 / b;
+    u64 x = 0;
+    for (; p * b < bit0 + 64; ++p) {
+        const u64 code = p < n ? ct.code[text[p]] : 0;
+        const long long off = p * b - bit0;  // bit offset of this code's MSB within the word (may be < 0)
+        const int sh = 64 - b - (int)off;     // left shift placing the code
+        if (sh >= 0) x |= code << sh;
+        else x |= code >> (-sh);
     }
-    __syncthreads();
-    long long i = base + threadIdx.x;
-    if (i >= n) return;
-    u64 key = 0;
-    for (int j = 0; j < K; ++j) key = (key << b) | s[threadIdx.x + j];
-    // Input order of the stable sort: the S = min(K-1, n) short suffixes
-    // (fewer than K symbols, padded) first by increasing length, then the rest
-    // by position -- so among equal padded keys a short suffix (a proper
-    // prefix of the others) precedes them, as the true order requires.
-    const long long S = (long long)K - 1 < n ? (long long)K - 1 : n;
-    const long long e = (n - i < K) ? n - 1 - i : i + S;
-    keys[e] = key;
-    vals[e] = (unsigned)i;
+    stream[w] = x;
 }
 
 // Round r >= 1 keys for the unsorted slots P[0..U).
@@ -472,10 +466,16 @@ void build_suffix_array(rs_ctx *c, long long n) {
     unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots(n));
     RS_CUDA(cudaMemsetAsync(raw, 0, sizeof(unsigned), c->stream));
 
-    RS_LAUNCH_B(c, 13.0 * n, k_init_keys, grid_for(n, 256), 256, 0, text, n, ct, bits, K, k0, v0);
+    // pack the text once (n*b/8 bytes, L2-resident at 256 Mi DNA); the sort's
+    // histogram and first pass generate (key, suffix) pairs from it directly.
+    const long long words = (n * bits + 63) / 64 + 4;
+    u64 *stream = (u64 *)buf(c, B_PACKED, sizeof(u64) * (size_t)words);
+    RS_LAUNCH_B(c, (double)n + 8.0 * words, k_pack_text, grid_for(words, 256), 256, 0, text, n, ct, bits, words,
+                stream);
+    const TextKeys tk{stream, n, bits, K, std::min<long long>(K - 1, n)};
     u64 *ks;
     unsigned *vs;
-    radix_sort_pairs(c, k0, k1, v0, v1, n, bits * K, &ks, &vs);
+    radix_sort_pairs(c, k0, k1, v0, v1, n, bits * K, &ks, &vs, &tk);
 
     long long U = n;
     const unsigned *P = nullptr;
