@@ -63,6 +63,10 @@ enum BufId {
     B_T5,
     B_PATCH,     // list of patched LCP slots
     B_PACKED,    // text packed as b-bit codes
+    B_H0,        // per-round unsorted group heads / suffixes (ping-pong)
+    B_H1,
+    B_V0,
+    B_V1,
     B_COUNT
 };
 

@@ -138,19 +138,38 @@ template <bool RAW, bool ALL>
 __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x) {
     const unsigned cnt = (unsigned)x.cnt;
     const int tile_k0 = (int)x.tile_k0, tile_k1 = (int)x.tile_k1;
-    for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
-        const int ep = t ? c.end(t - 1) : tile_k0 - 1;
-        const int e_t = c.end(t);
-        int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
-        int b = e_t < tile_k1 ? e_t : tile_k1;
+    if (cnt * 8 < (unsigned)x.npos) {
+        // few long candidates (repetitive text): one binary search per position
+        for (int p = threadIdx.x; p < x.npos; p += kNT) {
+            const int k = tile_k0 + p;
+            unsigned a = 0, b = cnt;
+            while (a < b) {
+                const unsigned mid = (a + b) >> 1;
+                if (c.end(mid) >= k) b = mid; else a = mid + 1;
+            }
+            x.s_lo[p] = a;
+            b = cnt;
+            while (a < b) {
+                const unsigned mid = (a + b) >> 1;
+                if ((int)c.start(mid) <= k) a = mid + 1; else b = mid;
+            }
+            x.s_hi[p] = a;
+        }
+    } else {
+        for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
+            const int ep = t ? c.end(t - 1) : tile_k0 - 1;
+            const int e_t = c.end(t);
+            int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
+            int b = e_t < tile_k1 ? e_t : tile_k1;
 #pragma unroll 1
-        for (int k = a; k <= b; ++k) x.s_lo[k - tile_k0] = t;
-        const int st = (int)c.start(t);
-        const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
-        a = st > tile_k0 ? st : tile_k0;
-        b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
+            for (int k = a; k <= b; ++k) x.s_lo[k - tile_k0] = t;
+            const int st = (int)c.start(t);
+            const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
+            a = st > tile_k0 ? st : tile_k0;
+            b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
 #pragma unroll 1
-        for (int k = a; k <= b; ++k) x.s_hi[k - tile_k0] = t + 1;
+            for (int k = a; k <= b; ++k) x.s_hi[k - tile_k0] = t + 1;
+        }
     }
     __syncthreads();
 

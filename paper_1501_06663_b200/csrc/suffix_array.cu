@@ -87,13 +87,13 @@ __global__ void k_pack_text(const unsigned char *__restrict__ text, long long n,
 }
 
 // Round r >= 1 keys for the unsorted slots P[0..U).
-__global__ void k_make_keys(const unsigned *__restrict__ P, long long U, const unsigned *__restrict__ sa,
+__global__ void k_make_keys(const unsigned *__restrict__ H, const unsigned *__restrict__ V, long long U,
                             const unsigned *__restrict__ isa, long long n, long long h,
                             u64 *__restrict__ keys, unsigned *__restrict__ vals) {
     long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (t >= U) return;
-    unsigned i = sa[P[t]];
-    u64 hi = isa[i];
+    const unsigned i = V[t];
+    const u64 hi = H[t];
     // Suffixes shorter than h (padded with the smallest code) order by length
     // before every longer member of their group: lo = remaining length in
     // [1, h]; otherwise h + 1 + rank of suffix i + h.
@@ -128,7 +128,8 @@ template <bool REDUCE>
 __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, const unsigned *__restrict__ vals,
                                                  const unsigned *__restrict__ P, long long U,
                                                  unsigned *__restrict__ sa, unsigned *__restrict__ isa,
-                                                 unsigned *__restrict__ P_next, u64 *__restrict__ tile_agg,
+                                                 unsigned *__restrict__ P_next, unsigned *__restrict__ H_next,
+                                                 unsigned *__restrict__ V_next, u64 *__restrict__ tile_agg,
                                                  const u64 *__restrict__ tile_prefix,
                                                  unsigned *__restrict__ lcp_d, int code_bits, int key_bits,
                                                  BucketEmit be) {
@@ -241,11 +242,24 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
         hh[j] = (unsigned)run;
         if (P) {
             sa[pos[j]] = v;
-            isa[v] = (unsigned)run;
+            if (!be.stage) isa[v] = (unsigned)run;
         }
-        if (unsorted >> j & 1) P_next[o++] = pos[j];
+        if (unsorted >> j & 1) {
+            // next round's inputs: slot, group head (= new isa) and suffix,
+            // so k_make_keys needs only the one random gather isa[i + h]
+            P_next[o] = pos[j];
+            H_next[o] = (unsigned)run;
+            V_next[o] = v;
+            ++o;
+        }
     }
-    if (P) return;
+    if (P) {
+        if (be.stage) {  // large later rounds: ISA through the bucketed scatter too
+            __syncthreads();
+            bucket_emit<kUNT, kUIPT>(be, vv, hh, s_emit);
+        }
+        return;
+    }
     // ---- round 0: SA slots are t itself -> coalesced stores through shared memory ----
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) s_stage[threadIdx.x * kUIPT + j] = vv[j];
@@ -460,6 +474,10 @@ void build_suffix_array(rs_ctx *c, long long n) {
     unsigned *v1 = (unsigned *)buf(c, B_VALS1, sizeof(unsigned) * (size_t)n);
     unsigned *Pa = (unsigned *)buf(c, B_T0, sizeof(unsigned) * (size_t)n);
     unsigned *Pb = (unsigned *)buf(c, B_T1, sizeof(unsigned) * (size_t)n);
+    unsigned *Ha = (unsigned *)buf(c, B_H0, sizeof(unsigned) * (size_t)n);
+    unsigned *Hb = (unsigned *)buf(c, B_H1, sizeof(unsigned) * (size_t)n);
+    unsigned *Va = (unsigned *)buf(c, B_V0, sizeof(unsigned) * (size_t)n);
+    unsigned *Vb = (unsigned *)buf(c, B_V1, sizeof(unsigned) * (size_t)n);
     unsigned long long *u_dev = (unsigned long long *)buf(c, B_SMALL, 4096) + 4;
     unsigned *lcp_d = (unsigned *)buf(c, B_LCP, sizeof(unsigned) * (size_t)(n + 4));
     RS_CUDA(cudaMemsetAsync(lcp_d + n, 0, sizeof(unsigned) * 4, c->stream));
@@ -489,24 +507,28 @@ void build_suffix_array(rs_ctx *c, long long n) {
         u64 *tpre = tagg + tiles + 1;
         BucketEmit be{nullptr, nullptr, 0, 0, nullptr};
         if (!P) be = bucket_setup(c, n, 0, true);
+        else if (U >= n / 16) be = bucket_setup(c, n, 0, false);
         // reduce-then-scan instead of a look-back: the heavy pass never waits
-        RS_LAUNCH_B(c, 8.0 * U, k_update<true>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, tagg, tpre,
-                    lcp_d, bits, bits * K, be);
+        RS_LAUNCH_B(c, 8.0 * U, k_update<true>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha, Va, tagg,
+                    tpre, lcp_d, bits, bits * K, be);
         RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
         // round 0: 12 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
         RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, k_update<false>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa,
-                    tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
+                    Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
         add_bytes_last(c, 4.0 * (double)un);
         if (!P) bucket_apply(c, be, isa, n, raw, 1);
+        else if (be.stage) bucket_apply(c, be, isa, U);
         U = (long long)un;
         if (c->sa_rounds == 1) c->sa_unsorted_after_round0 = U;
         if (U == 0) break;
         if (depth >= n) fail(RS_ECUDA, "suffix sort did not converge");
-        std::swap(Pa, Pb);  // Pb now holds the unsorted list
+        std::swap(Pa, Pb);  // Pb/Hb/Vb now hold the unsorted slots, heads, suffixes
+        std::swap(Ha, Hb);
+        std::swap(Va, Vb);
         P = Pb;
-        RS_LAUNCH_B(c, 28.0 * U, k_make_keys, grid_for(U, 256), 256, 0, P, U, sa, isa, n, depth, k0, v0);
+        RS_LAUNCH_B(c, 20.0 * U, k_make_keys, grid_for(U, 256), 256, 0, Hb, Vb, U, isa, n, depth, k0, v0);
         // bits of a round key hi*(n+h+1)+lo < n*(n+h+1)
         int rbits = (int)std::ceil(std::log2((double)n * (double)(n + depth + 1)));
         if (rbits < 1) rbits = 1;
