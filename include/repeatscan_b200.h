@@ -153,6 +153,15 @@ int rs_profile_kernel(rs_ctx *ctx, int i, char *name, int cap, int64_t *launches
 /* Number of prefix-doubling rounds of the last on-device suffix sort. */
 int rs_sa_rounds(const rs_ctx *ctx, int *rounds);
 
+/* ---- walk-step statistics (stats.py:21-76) ---------------
+ * Steps of the raw / compact query walk at every position (= candidates
+ * covering it) for the loaded raw array or compact entries: steps[n+1]
+ * (may be NULL), stats[4] = {min, max, sum, count} over positions with
+ * steps > 0 (min = 0 when count = 0). */
+int rs_walk_steps(rs_ctx *ctx, int path, int64_t *steps, int64_t *stats);
+/* summarize_steps (stats.py:58-68) of a caller-given steps array of `count` values. */
+int rs_summarize_steps(rs_ctx *ctx, const int64_t *steps, int64_t count, int64_t *stats);
+
 /* ---- sharded query (multi-GPU) ------------------------------
  * One process per GPU.  The compact entries of the WHOLE text live in every
  * rank's device buffer (rank 0 builds them, torch.distributed/NCCL broadcasts

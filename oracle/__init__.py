@@ -239,3 +239,36 @@ def brute_all_positions(s: bytes, mode: str = "leftmost"):
         hits = [(i, best) for i in range(1, k + 1) if reach[i] >= best and i + best - 1 >= k]
         out.append(hits[0] if mode == "leftmost" else hits)
     return out
+
+
+# -- stats.py:30-68 walk-step statistics (numpy closed form) --------------------
+def walk_steps_raw(raw: np.ndarray) -> np.ndarray:
+    """stats.py:30-43: steps[k] = k - #{i : i + raw[i] - 1 < k}."""
+    n = int(raw.size) - 1
+    steps = np.zeros(n + 1, dtype=np.int64)
+    if n == 0:
+        return steps
+    ends = np.arange(1, n + 1, dtype=np.int64) + raw[1:] - 1
+    ks = np.arange(1, n + 1, dtype=np.int64)
+    steps[1:] = ks - np.searchsorted(ends, ks, side="left")
+    return steps
+
+
+def walk_steps_compact(starts: np.ndarray, lengths: np.ndarray, n: int) -> np.ndarray:
+    """stats.py:46-55: max(#starts <= k - #ends < k, 0)."""
+    steps = np.zeros(n + 1, dtype=np.int64)
+    if n == 0 or starts.size == 0:
+        return steps
+    ends = starts + lengths - 1
+    ks = np.arange(1, n + 1, dtype=np.int64)
+    steps[1:] = np.maximum(np.searchsorted(starts, ks, side="right")
+                           - np.searchsorted(ends, ks, side="left"), 0)
+    return steps
+
+
+def summarize_steps(steps: np.ndarray):
+    """stats.py:58-68 -> (min, max, avg, positions)."""
+    covered = steps[steps > 0]
+    if covered.size == 0:
+        return 0, 0, 0.0, 0
+    return int(covered.min()), int(covered.max()), float(covered.mean()), int(covered.size)

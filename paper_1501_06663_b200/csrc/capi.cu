@@ -25,6 +25,8 @@ void scatter_i64(rs_ctx *c, const long long *d_raw, const long long *d_flags, co
                  long long n, long long m, long long *d_starts, long long *d_lengths);
 bool verify_structures(rs_ctx *c, const unsigned char *d_text, long long n, const long long *d_sa,
                        const long long *d_rank, const long long *d_lcp);
+void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned long long *acc_host);
+void summarize(rs_ctx *c, const long long *d_steps, long long count, unsigned long long *acc_host);
 void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
                  long long kb, long long ke, int out_off, long long n_slots);
 
@@ -766,6 +768,47 @@ int rs_suffix_structures(rs_ctx *c, const uint8_t *text, int64_t n, int64_t *sa,
     rc = rs_build_structures(c);
     if (rc) return rc;
     return rs_get_structures(c, sa, rank, lcp);
+}
+
+// ---- walk statistics ---------------------------------------------------------------
+
+static void stats_out(const unsigned long long *acc, int64_t *stats) {
+    stats[0] = acc[3] ? (int64_t)acc[0] : 0;
+    stats[1] = (int64_t)acc[1];
+    stats[2] = (int64_t)acc[2];
+    stats[3] = (int64_t)acc[3];
+}
+
+int rs_walk_steps(rs_ctx *c, int path, int64_t *steps, int64_t *stats) {
+    return guarded(c, [&] {
+        if (path != RS_PATH_RAW && path != RS_PATH_COMPACT) fail(RS_EINVAL, "unknown path");
+        if (!stats) fail(RS_EINVAL, "stats output required");
+        if (c->n < 0) fail(RS_ESTATE, "nothing loaded");
+        bool used[RS_NUM_STAGES] = {};
+        if (path == RS_PATH_RAW) ensure_raw(c, used);
+        else ensure_compact(c, used);
+        long long n = c->n;
+        long long *d = nullptr;
+        if (steps) d = (long long *)buf(c, B_I64C, 8 * (size_t)(n + 1));
+        unsigned long long acc[4];
+        walk_steps(c, path, n, d, acc);
+        if (steps) {
+            d2h(c, steps, d, 8 * (size_t)(n + 1));
+            RS_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        stats_out(acc, stats);
+    });
+}
+
+int rs_summarize_steps(rs_ctx *c, const int64_t *steps, int64_t count, int64_t *stats) {
+    return guarded(c, [&] {
+        if (count < 0 || !stats) fail(RS_EINVAL, "bad arguments");
+        long long *d = (long long *)buf(c, B_I64C, 8 * (size_t)(count + 1));
+        h2d(c, d, steps, 8 * (size_t)count);
+        unsigned long long acc[4];
+        summarize(c, d, count, acc);
+        stats_out(acc, stats);
+    });
 }
 
 // ---- sharded ---------------------------------------------------------------------

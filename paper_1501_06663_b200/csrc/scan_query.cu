@@ -17,6 +17,8 @@
 // variant is single-pass: per-position tie counts -> block scan -> decoupled
 // look-back for the tile's global CSR base -> offsets and tie starts written
 // directly in the reference int64 layout.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rsb {
@@ -121,6 +123,50 @@ __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict
     bounds[2 * g + 1] = hi;
 }
 
+// Window bounds per position: every position's window is the contiguous
+// candidate range [lo(k), hi(k)); lo(k) = first candidate with end >= k,
+// hi(k) = #candidates with start <= k.  Both are nondecreasing, so each
+// candidate fills the positions where it is the boundary -- O(tile +
+// candidates), no searches -- unless candidates are few and long
+// (repetitive text), then one binary search per position.
+template <bool RAW>
+__device__ __forceinline__ void fill_windows(const Cand<RAW> &c, unsigned cnt, int tile_k0, int tile_k1, int npos,
+                                             unsigned *s_lo, unsigned *s_hi) {
+    if (cnt * 8 < (unsigned)npos) {
+        for (int p = threadIdx.x; p < npos; p += kNT) {
+            const int k = tile_k0 + p;
+            unsigned a = 0, b = cnt;
+            while (a < b) {
+                const unsigned mid = (a + b) >> 1;
+                if (c.end(mid) >= k) b = mid; else a = mid + 1;
+            }
+            s_lo[p] = a;
+            b = cnt;
+            while (a < b) {
+                const unsigned mid = (a + b) >> 1;
+                if ((int)c.start(mid) <= k) a = mid + 1; else b = mid;
+            }
+            s_hi[p] = a;
+        }
+    } else {
+        for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
+            const int ep = t ? c.end(t - 1) : tile_k0 - 1;
+            const int e_t = c.end(t);
+            int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
+            int b = e_t < tile_k1 ? e_t : tile_k1;
+#pragma unroll 1
+            for (int k = a; k <= b; ++k) s_lo[k - tile_k0] = t;
+            const int st = (int)c.start(t);
+            const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
+            a = st > tile_k0 ? st : tile_k0;
+            b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
+#pragma unroll 1
+            for (int k = a; k <= b; ++k) s_hi[k - tile_k0] = t + 1;
+        }
+    }
+    __syncthreads();
+}
+
 struct TileCtx {
     long long tile, cnt, tile_k0, tile_k1, slot0, tiles, flat_cap;
     int npos, out_off;
@@ -137,41 +183,7 @@ struct TileCtx {
 template <bool RAW, bool ALL>
 __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x) {
     const unsigned cnt = (unsigned)x.cnt;
-    const int tile_k0 = (int)x.tile_k0, tile_k1 = (int)x.tile_k1;
-    if (cnt * 8 < (unsigned)x.npos) {
-        // few long candidates (repetitive text): one binary search per position
-        for (int p = threadIdx.x; p < x.npos; p += kNT) {
-            const int k = tile_k0 + p;
-            unsigned a = 0, b = cnt;
-            while (a < b) {
-                const unsigned mid = (a + b) >> 1;
-                if (c.end(mid) >= k) b = mid; else a = mid + 1;
-            }
-            x.s_lo[p] = a;
-            b = cnt;
-            while (a < b) {
-                const unsigned mid = (a + b) >> 1;
-                if ((int)c.start(mid) <= k) a = mid + 1; else b = mid;
-            }
-            x.s_hi[p] = a;
-        }
-    } else {
-        for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
-            const int ep = t ? c.end(t - 1) : tile_k0 - 1;
-            const int e_t = c.end(t);
-            int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
-            int b = e_t < tile_k1 ? e_t : tile_k1;
-#pragma unroll 1
-            for (int k = a; k <= b; ++k) x.s_lo[k - tile_k0] = t;
-            const int st = (int)c.start(t);
-            const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
-            a = st > tile_k0 ? st : tile_k0;
-            b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
-#pragma unroll 1
-            for (int k = a; k <= b; ++k) x.s_hi[k - tile_k0] = t + 1;
-        }
-    }
-    __syncthreads();
+    fill_windows<RAW>(c, cnt, (int)x.tile_k0, (int)x.tile_k1, x.npos, x.s_lo, x.s_hi);
 
     // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
     unsigned best[kPPT];
@@ -353,6 +365,99 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     }
 }
 
+// Walk-step statistics (stats.py:30-76): the steps of a query walk at k are
+// exactly the candidates covering k, i.e. the window size hi(k) - lo(k)
+// (raw: k - #{i : i + raw[i] - 1 < k}; compact: max(upto - below, 0)).
+// Writes steps[k] (optional) and accumulates min/max/sum/count over k with
+// steps > 0 into acc[4].
+template <bool RAW>
+__global__ void __launch_bounds__(kNT) k_steps(const uint2 *__restrict__ e, const unsigned *__restrict__ raw,
+                                               long long kb, long long ke, const long long *__restrict__ bounds,
+                                               long long *__restrict__ steps, unsigned long long *acc) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    unsigned char *s_stage = dsm;
+    unsigned *s_lo = reinterpret_cast<unsigned *>(dsm + kStageBytes);
+    unsigned *s_hi = s_lo + kG;
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ unsigned long long s_red[4];
+    const long long tile = blockIdx.x;
+    const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];
+    const long long cnt = hi - lo;
+    const long long tile_k0 = kb + tile * kG;
+    const int npos = (int)((ke - tile_k0 + 1) < kG ? (ke - tile_k0 + 1) : kG);
+    if (threadIdx.x < 4) s_red[threadIdx.x] = threadIdx.x == 0 ? ~0ull : 0ull;
+    for (int i = threadIdx.x; i < npos; i += kNT) {
+        s_lo[i] = (unsigned)cnt;
+        s_hi[i] = 0;
+    }
+    const int esz = RAW ? 4 : 8;
+    const long long align = 16 / esz;
+    const long long a = lo & ~(align - 1), b = (hi + align - 1) & ~(align - 1);
+    const bool fits = cnt > 0 && b - a <= (RAW ? kCapR : kCapC);
+    if (fits && threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        unsigned bytes = (unsigned)((b - a) * esz);
+        mbar_expect_tx(&s_bar, bytes);
+        tma_load_1d(s_stage, RAW ? (const void *)(raw + a) : (const void *)(e + a), bytes, &s_bar);
+    }
+    __syncthreads();
+    Cand<RAW> c;
+    c.base = (unsigned)lo;
+    if (fits) {
+        mbar_wait(&s_bar, 0);
+        c.e = RAW ? nullptr : reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
+        c.r = RAW ? reinterpret_cast<const unsigned *>(s_stage) + (lo - a) : nullptr;
+    } else {
+        c.e = RAW ? nullptr : e + lo;
+        c.r = RAW ? raw + lo : nullptr;
+    }
+    fill_windows<RAW>(c, (unsigned)(cnt > 0 ? cnt : 0), (int)tile_k0, (int)(tile_k0 + npos - 1), npos, s_lo, s_hi);
+    unsigned long long mn = ~0ull, mx = 0, sum = 0, n = 0;
+    for (int p = threadIdx.x; p < npos; p += kNT) {
+        const long long w = (long long)s_hi[p] - (long long)s_lo[p];
+        const unsigned long long st = w > 0 ? (unsigned long long)w : 0ull;
+        if (steps) steps[tile_k0 + p] = (long long)st;
+        if (st) {
+            mn = st < mn ? st : mn;
+            mx = st > mx ? st : mx;
+            sum += st;
+            ++n;
+        }
+    }
+    atomicMin(&s_red[0], mn);
+    atomicMax(&s_red[1], mx);
+    atomicAdd(&s_red[2], sum);
+    atomicAdd(&s_red[3], n);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMin(&acc[0], s_red[0]);
+        atomicMax(&acc[1], s_red[1]);
+        atomicAdd(&acc[2], s_red[2]);
+        atomicAdd(&acc[3], s_red[3]);
+    }
+}
+
+// Summary of a caller-given steps array (summarize_steps, stats.py:58-68).
+__global__ void k_summarize(const long long *__restrict__ steps, long long n, unsigned long long *acc) {
+    unsigned long long mn = ~0ull, mx = 0, sum = 0, cnt = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long v = steps[i];
+        if (v > 0) {
+            const unsigned long long u = (unsigned long long)v;
+            mn = u < mn ? u : mn;
+            mx = u > mx ? u : mx;
+            sum += u;
+            ++cnt;
+        }
+    }
+    if (cnt) {
+        atomicMin(&acc[0], mn);
+        atomicMax(&acc[1], mx);
+        atomicAdd(&acc[2], sum);
+        atomicAdd(&acc[3], cnt);
+    }
+}
+
 }  // namespace
 
 // Run the scan for positions [kb, ke] over candidates (compact entries or raw),
@@ -419,6 +524,49 @@ void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
         cap_slots = (size_t)T + 64;
     }
     fail(RS_ECUDA, "tie buffer sizing did not converge");
+}
+
+// Walk steps / statistics over positions [1, n] of the loaded candidates.
+// steps_out: device int64[n+1] or null; acc_host receives {min, max, sum, count}.
+void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned long long *acc_host) {
+    const bool rawp = path == RS_PATH_RAW;
+    unsigned long long *acc = (unsigned long long *)buf(c, B_SMALL, 4096) + 16;
+    unsigned long long init[4] = {~0ull, 0, 0, 0};
+    RS_CUDA(cudaMemcpyAsync(acc, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    if (d_steps) RS_CUDA(cudaMemsetAsync(d_steps, 0, sizeof(long long), c->stream));
+    if (n > 0) {
+        const uint2 *d_e = (const uint2 *)c->bufs[B_LLRC].p;
+        const unsigned *d_raw = (const unsigned *)c->bufs[B_RAW].p;
+        const long long count = rawp ? 0 : c->m;
+        long long tiles = (n + kG - 1) / kG;
+        long long *bounds = (long long *)buf(c, B_BOUNDS, sizeof(long long) * 2 * (size_t)tiles);
+        static bool attr = false;
+        if (!attr) {
+            const int sm = kStageBytes + 2 * 4 * kG;
+            RS_CUDA(cudaFuncSetAttribute(k_steps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            RS_CUDA(cudaFuncSetAttribute(k_steps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            attr = true;
+        }
+        const int sm = kStageBytes + 2 * 4 * kG;
+        if (rawp) {
+            RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds);
+            RS_LAUNCH(c, k_steps<true>, (unsigned)tiles, kNT, sm, d_e, d_raw, 1, n, bounds, d_steps, acc);
+        } else {
+            RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds);
+            RS_LAUNCH(c, k_steps<false>, (unsigned)tiles, kNT, sm, d_e, d_raw, 1, n, bounds, d_steps, acc);
+        }
+    }
+    fetch_small(c, acc_host, acc, 4 * sizeof(unsigned long long));
+}
+
+void summarize(rs_ctx *c, const long long *d_steps, long long count, unsigned long long *acc_host) {
+    unsigned long long *acc = (unsigned long long *)buf(c, B_SMALL, 4096) + 16;
+    unsigned long long init[4] = {~0ull, 0, 0, 0};
+    RS_CUDA(cudaMemcpyAsync(acc, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    if (count > 0)
+        RS_LAUNCH(c, k_summarize, (unsigned)std::min<long long>(grid_for(count, 256), (long long)c->sm_count * 8), 256, 0,
+                  d_steps, count, acc);
+    fetch_small(c, acc_host, acc, 4 * sizeof(unsigned long long));
 }
 
 }  // namespace rsb

@@ -280,3 +280,41 @@ def test_distributed_single_rank_nccl():
         assert np.array_equal(res.starts, ws) and np.array_equal(res.lengths, wln)
     finally:
         dist.destroy_process_group()
+
+
+def test_walk_stats_vs_closed_form():
+    # stats.py:30-76 (reference closed form restated in oracle/) on the golden
+    # inputs and on structured texts; plus the reference's own known answers.
+    for c in golden_cases()[::2] + [None]:
+        if c is None:
+            data = workloads.fibonacci_mutated(200_000, 5, rate=1e-3)
+            sa, rank, lcp = oracle.build_suffix_structures(data)
+            raw = oracle.build_raw_llr(rank, lcp)
+            cs, cl = oracle.build_compact_llr(raw)
+        else:
+            raw, cs, cl = c.raw, c.c_starts, c.c_lengths
+        n = raw.size - 1
+        comp = rb.CompactLlr.from_arrays(cs, cl)
+        wr = oracle.walk_steps_raw(raw)
+        wc = oracle.walk_steps_compact(cs, cl, n)
+        from paper_1501_06663_b200 import stats as S
+        assert np.array_equal(S.walk_steps_raw(raw), wr)
+        assert np.array_equal(S.walk_steps_compact(comp, n), wc)
+        for path, w in (("raw", wr), ("compact", wc)):
+            got = rb.compute_walk_stats(raw, comp, path)
+            mn, mx, avg, pos = oracle.summarize_steps(w)
+            assert (got.min_steps, got.max_steps, got.positions) == (mn, mx, pos)
+            assert got.avg_steps == pytest.approx(avg, rel=1e-12)
+            s2 = S.summarize_steps(w, path)
+            assert (s2.min_steps, s2.max_steps, s2.positions) == (mn, mx, pos)
+    raw = rb.build_raw_llr(rb.build_suffix_structures(rb.Text.from_str("aaaa")))
+    from paper_1501_06663_b200 import stats as S
+    assert S.walk_steps_raw(raw)[1:].tolist() == [1, 2, 3, 3]  # test_stats.py:18-23
+    st = rb.compute_walk_stats(raw, rb.compact_llr_sequential(raw), "raw")
+    assert (st.min_steps, st.max_steps) == (1, 3) and st.avg_steps == (1 + 2 + 3 + 3) / 4
+    raw = rb.build_raw_llr(rb.build_suffix_structures(rb.Text.from_str("abc")))
+    for path in ("raw", "compact"):  # test_stats.py:26-30
+        st = rb.compute_walk_stats(raw, rb.compact_llr_sequential(raw), path)
+        assert (st.min_steps, st.max_steps, st.avg_steps, st.positions) == (0, 0, 0.0, 0)
+    with pytest.raises(ValueError):
+        rb.compute_walk_stats(raw, rb.compact_llr_sequential(raw), "bogus")
