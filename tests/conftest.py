@@ -25,7 +25,8 @@ class GoldenCase:
 
     def __init__(self, z, i):
         for f in ("text", "sa", "rank", "lcp", "raw", "flags", "ps", "c_starts",
-                  "c_lengths", "l_starts", "l_lengths", "a_lengths", "a_offsets", "a_flat"):
+                  "c_lengths", "l_starts", "l_lengths", "a_lengths", "a_offsets", "a_flat",
+                  "w_raw", "w_comp"):
             off = z[f + "_off"]
             setattr(self, f, z[f][off[i]:off[i + 1]])
         self.data = self.text.astype(np.uint8)

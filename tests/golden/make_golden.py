@@ -45,7 +45,7 @@ assert "reference" in repeatscan.__file__ or "/root/reference" in repeatscan.__f
     repeatscan.__file__
 
 FIELDS = ("text", "sa", "rank", "lcp", "raw", "flags", "ps", "c_starts", "c_lengths",
-          "l_starts", "l_lengths", "a_lengths", "a_offsets", "a_flat")
+          "l_starts", "l_lengths", "a_lengths", "a_offsets", "a_flat", "w_raw", "w_comp")
 
 
 def reference_arrays(data: np.ndarray, paths=("raw", "compact"), policy=None) -> dict:
@@ -71,6 +71,8 @@ def reference_arrays(data: np.ndarray, paths=("raw", "compact"), policy=None) ->
             assert np.array_equal(alll.flat_starts, A.flat_starts)
     out.update(l_starts=left.starts, l_lengths=left.lengths, a_lengths=alll.lengths,
                a_offsets=alll.offsets, a_flat=alll.flat_starts)
+    from repeatscan.stats import walk_steps_compact, walk_steps_raw  # stats.py:30-55
+    out.update(w_raw=walk_steps_raw(raw), w_comp=walk_steps_compact(c, s.n))
     return out
 
 

@@ -295,8 +295,8 @@ def test_walk_stats_vs_closed_form():
             raw, cs, cl = c.raw, c.c_starts, c.c_lengths
         n = raw.size - 1
         comp = rb.CompactLlr.from_arrays(cs, cl)
-        wr = oracle.walk_steps_raw(raw)
-        wc = oracle.walk_steps_compact(cs, cl, n)
+        wr = oracle.walk_steps_raw(raw) if c is None else c.w_raw      # golden: the reference's own
+        wc = oracle.walk_steps_compact(cs, cl, n) if c is None else c.w_comp
         from paper_1501_06663_b200 import stats as S
         assert np.array_equal(S.walk_steps_raw(raw), wr)
         assert np.array_equal(S.walk_steps_compact(comp, n), wc)

@@ -121,3 +121,10 @@ def test_oracle_matches_reference_digests(name):
     assert digest(af) == rec["a_flat"]
     st, ln = oracle.leftmost_all_positions(data.size, "compact", raw, (s, l), 0)
     assert digest(st) == rec["l_starts"] and digest(ln) == rec["l_lengths"]
+
+
+def test_oracle_walk_stats_match_reference_golden():
+    # stats.py:30-55 restated in oracle/ vs the reference's own arrays
+    for c in golden_cases():
+        assert np.array_equal(oracle.walk_steps_raw(c.raw), c.w_raw), c
+        assert np.array_equal(oracle.walk_steps_compact(c.c_starts, c.c_lengths, c.n), c.w_comp), c
