@@ -153,6 +153,13 @@ int rs_profile_kernel(rs_ctx *ctx, int i, char *name, int cap, int64_t *launches
 /* Number of prefix-doubling rounds of the last on-device suffix sort. */
 int rs_sa_rounds(const rs_ctx *ctx, int *rounds);
 
+/* ---- TSV wire format (cli.py:62-93) ------------------------
+ * Serialize positions [lo, hi] (1-based, inclusive) of the last rs_query
+ * result on device, byte-identical to the reference CLI; *nbytes receives the
+ * size; rs_fetch_serialized copies the bytes out. */
+int rs_serialize(rs_ctx *ctx, int64_t lo, int64_t hi, int64_t *nbytes);
+int rs_fetch_serialized(rs_ctx *ctx, uint8_t *out);
+
 /* ---- walk-step statistics (stats.py:21-76) ---------------
  * Steps of the raw / compact query walk at every position (= candidates
  * covering it) for the loaded raw array or compact entries: steps[n+1]

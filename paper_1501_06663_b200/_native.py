@@ -71,6 +71,8 @@ SIGNATURES = {
     "rs_profile_kernel": [_CTX, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, _I64P,
                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
     "rs_sa_rounds": [_CTX, ctypes.POINTER(ctypes.c_int)],
+    "rs_serialize": [_CTX, ctypes.c_int64, ctypes.c_int64, _I64P],
+    "rs_fetch_serialized": [_CTX, _U8P],
     "rs_walk_steps": [_CTX, ctypes.c_int, _I64P, _I64P],
     "rs_summarize_steps": [_CTX, _I64P, ctypes.c_int64, _I64P],
     "rs_device_buffer": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(_VP)],

@@ -25,6 +25,7 @@ void scatter_i64(rs_ctx *c, const long long *d_raw, const long long *d_flags, co
                  long long n, long long m, long long *d_starts, long long *d_lengths);
 bool verify_structures(rs_ctx *c, const unsigned char *d_text, long long n, const long long *d_sa,
                        const long long *d_rank, const long long *d_lcp);
+long long serialize_tsv(rs_ctx *c, int mode, long long lo, long long hi);
 void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned long long *acc_host);
 void summarize(rs_ctx *c, const long long *d_steps, long long count, unsigned long long *acc_host);
 void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
@@ -630,9 +631,12 @@ int rs_query(rs_ctx *c, int mode, int path, int64_t *total) {
                 if (mode == RS_MODE_ALL) h2d(c, o1 + 1, z + 1, 8);
                 c->total = 0;
                 c->out_mode = mode;
+                c->out_ref_layout = true;
             } else if (path == RS_PATH_RAW) {
+                c->out_ref_layout = true;
                 query_range(c, mode, path, nullptr, 0, (const unsigned *)c->bufs[B_RAW].p, 1, n, 1, n);
             } else {
+                c->out_ref_layout = true;
                 query_range(c, mode, path, (const uint2 *)c->bufs[B_LLRC].p, c->m, nullptr, 1, n, 1, n);
             }
         }
@@ -770,6 +774,27 @@ int rs_suffix_structures(rs_ctx *c, const uint8_t *text, int64_t n, int64_t *sa,
     return rs_get_structures(c, sa, rank, lcp);
 }
 
+// ---- TSV ---------------------------------------------------------------------------
+
+int rs_serialize(rs_ctx *c, int64_t lo, int64_t hi, int64_t *nbytes) {
+    return guarded(c, [&] {
+        if (c->out_mode != RS_MODE_LEFTMOST && c->out_mode != RS_MODE_ALL) fail(RS_ESTATE, "no query results");
+        if (!c->out_ref_layout) fail(RS_ESTATE, "shard-local results are not serializable");
+        if (lo < 1 || hi > c->n || (hi < lo && !(hi == lo - 1))) fail(RS_ERANGE, "range out of range");
+        *nbytes = serialize_tsv(c, c->out_mode, lo, hi);
+        if (hi < lo) c->tsv_bytes = 0;
+    });
+}
+
+int rs_fetch_serialized(rs_ctx *c, uint8_t *out) {
+    return guarded(c, [&] {
+        if (c->tsv_bytes > 0) {
+            d2h(c, out, c->bufs[B_TSV].p, (size_t)c->tsv_bytes);
+            RS_CUDA(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
 // ---- walk statistics ---------------------------------------------------------------
 
 static void stats_out(const unsigned long long *acc, int64_t *stats) {
@@ -856,6 +881,7 @@ int rs_query_shard(rs_ctx *c, int mode, int64_t lo, int64_t hi, int64_t *total) 
             RS_CUDA(cudaMemsetAsync(o1, 0, 8, c->stream));
             c->total = 0;
             c->out_mode = mode;
+            c->out_ref_layout = false;
             if (cnt > 0)
                 query_range(c, mode, RS_PATH_COMPACT, (const uint2 *)c->bufs[B_LLRC].p, c->m, nullptr, lo, hi - 1,
                             0, cnt);

@@ -63,6 +63,7 @@ enum BufId {
     B_T5,
     B_PATCH,     // list of patched LCP slots
     B_PACKED,    // text packed as b-bit codes
+    B_TSV,       // serialized TSV bytes
     B_H0,        // per-round unsorted group heads / suffixes (ping-pong)
     B_H1,
     B_V0,
@@ -105,7 +106,9 @@ struct rs_ctx {
     long long sa_final_depth = 0;          // sorted depth when prefix doubling stopped
     bool lcp_from_keys = false;
     bool sa_device_built = false;
-    bool raw_from_round0 = false;           // B_RAW filled during the SA build (+ LCP patch fix-up)           // SA/ISA/LCP built here (mutually consistent)             // B_LCP holds round-0 key LCPs (+ unknown marks)
+    bool raw_from_round0 = false;
+    long long tsv_bytes = 0;
+    bool out_ref_layout = false;            // B_OUT* hold the reference 1-based layout           // B_RAW filled during the SA build (+ LCP patch fix-up)           // SA/ISA/LCP built here (mutually consistent)             // B_LCP holds round-0 key LCPs (+ unknown marks)
     // per-kernel profiling (CUDA events around every launch while enabled)
     bool profiling = false;
     struct ProfRec {
