@@ -371,8 +371,9 @@ __device__ __forceinline__ long long text_pos(const TextKeys &tk, long long e) {
 }
 // Sorts (keys, vals) pairs by the low `bits` bits of keys, stable.  With tk,
 // the input pairs are generated from the packed text (keys/vals unread).
-void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsigned *vals_alt,
-                      long long count, int bits, u64 **keys_out, unsigned **vals_out,
+template <typename KeyT>
+void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, unsigned *vals_alt,
+                      long long count, int bits, KeyT **keys_out, unsigned **vals_out,
                       const TextKeys *tk = nullptr);
 
 }  // namespace rsb

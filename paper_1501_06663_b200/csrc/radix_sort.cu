@@ -24,8 +24,8 @@ constexpr int kTile = kNT * kIPT;  // 3072 pairs per tile
 constexpr int kWarps = kNT / 32;
 constexpr int kRadix = 256;
 
-template <bool TEXT>
-__global__ void __launch_bounds__(kNT) k_histograms(const u64 *__restrict__ keys, long long count, int passes,
+template <bool TEXT, typename KeyT>
+__global__ void __launch_bounds__(kNT) k_histograms(const KeyT *__restrict__ keys, long long count, int passes,
                                                     unsigned long long *__restrict__ hist /*[passes][256]*/,
                                                     TextKeys tk) {
     __shared__ unsigned s_hist[8][kRadix];
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kNT) k_histograms(const u64 *__restrict__ keys
     __syncthreads();
     long long stride = (long long)gridDim.x * kNT;
     for (long long i = blockIdx.x * (long long)kNT + threadIdx.x; i < count; i += stride) {
-        u64 k = TEXT ? text_key(tk, i) : keys[i];  // histograms need no particular order
+        u64 k = TEXT ? text_key(tk, i) : (u64)keys[i];  // histograms need no particular order
         for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
     }
     __syncthreads();
@@ -59,16 +59,18 @@ __global__ void k_hist_scan(unsigned long long *hist) {
 }
 
 // (key, suffix) pairs straight from the packed text, in sort input order.
-__global__ void k_materialize(TextKeys tk, long long count, u64 *__restrict__ keys, unsigned *__restrict__ vals) {
+template <typename KeyT>
+__global__ void k_materialize(TextKeys tk, long long count, KeyT *__restrict__ keys, unsigned *__restrict__ vals) {
     long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= count) return;
     const long long pos = text_pos(tk, e);
-    keys[e] = text_key(tk, pos);
+    keys[e] = (KeyT)text_key(tk, pos);
     vals[e] = (unsigned)pos;
 }
 
+template <typename KeyT>
 struct SortSmem {
-    u64 keys[kTile];
+    KeyT keys[kTile];
     unsigned vals[kTile];
     unsigned short warp_cnt[kWarps][kRadix];  // per-warp digit counts, then warp offsets
     unsigned tile_start[kRadix];              // exclusive scan of tile digit counts
@@ -77,14 +79,14 @@ struct SortSmem {
     unsigned tile_id;
 };
 
-template <bool TEXT>
-__global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
-                                                  u64 *__restrict__ keys_out, unsigned *__restrict__ vals_out,
+template <bool TEXT, typename KeyT>
+__global__ void __launch_bounds__(kNT, 3) k_onesweep(const KeyT *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
+                                                  KeyT *__restrict__ keys_out, unsigned *__restrict__ vals_out,
                                                   long long count, int shift,
                                                   const unsigned long long *__restrict__ digit_base,
                                                   unsigned *counter, u64 *status /*[tiles][256]*/, TextKeys tk) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
+    SortSmem<KeyT> &sm = *reinterpret_cast<SortSmem<KeyT> *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kWarps * kRadix; i += kNT) (&sm.warp_cnt[0][0])[i] = 0;
     sm.hist[threadIdx.x] = 0;
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
     const long long tile = sm.tile_id;
     const long long base = tile * kTile + (long long)warp * (kIPT * 32);
 
-    u64 k[kIPT];
+    KeyT k[kIPT];
     unsigned v[kIPT];
     unsigned short rank[kIPT];
 #pragma unroll
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
         if (idx < count) {
             if (TEXT) {  // first pass of the round-0 sort: pairs straight from the packed text
                 const long long pos = text_pos(tk, idx);
-                k[i] = text_key(tk, pos);
+                k[i] = (KeyT)text_key(tk, pos);
                 v[i] = (unsigned)pos;
             } else {
                 k[i] = keys_in[idx];
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
     long long tile_count = count - tile * kTile;
     if (tile_count > kTile) tile_count = kTile;
     for (int j = threadIdx.x; j < tile_count; j += kNT) {
-        u64 key = sm.keys[j];
+        KeyT key = sm.keys[j];
         unsigned d = (unsigned)(key >> shift) & 0xff;
         unsigned long long dst = sm.global_base[d] + (j - sm.tile_start[d]);
         keys_out[dst] = key;
@@ -209,13 +211,14 @@ __global__ void __launch_bounds__(kNT, 3) k_onesweep(const u64 *__restrict__ key
 
 }  // namespace
 
-void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsigned *vals_alt,
-                      long long count, int bits, u64 **keys_out, unsigned **vals_out, const TextKeys *tk) {
+template <typename KeyT>
+void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, unsigned *vals_alt,
+                      long long count, int bits, KeyT **keys_out, unsigned **vals_out, const TextKeys *tk) {
     const TextKeys tkv = tk ? *tk : TextKeys{nullptr, 0, 0, 0, 0};
     *keys_out = keys;
     *vals_out = vals;
     if (count <= 1 || bits <= 0) {
-        if (tk && count > 0) RS_LAUNCH(c, k_materialize, grid_for(count, 256), 256, 0, tkv, count, keys, vals);
+        if (tk && count > 0) RS_LAUNCH(c, k_materialize<KeyT>, grid_for(count, 256), 256, 0, tkv, count, keys, vals);
         return;
     }
     int passes = (bits + 7) / 8;
@@ -224,9 +227,9 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
     RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
     unsigned hist_blocks = (unsigned)std::min<long long>((count + kNT * 16 - 1) / (kNT * 16), c->sm_count * 8);
     if (tk)
-        RS_LAUNCH_B(c, 0.25 * count, k_histograms<true>, hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+        RS_LAUNCH_B(c, 0.25 * count, (k_histograms<true, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
     else
-        RS_LAUNCH_B(c, 8.0 * count, k_histograms<false>, hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+        RS_LAUNCH_B(c, (double)sizeof(KeyT) * count, (k_histograms<false, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
     // Host needs the histograms to skip constant-digit passes.
     std::vector<unsigned long long> h((size_t)passes * kRadix);
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
@@ -234,14 +237,14 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
 
     static bool attr_set = false;
     if (!attr_set) {
-        RS_CUDA(cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(SortSmem)));
-        RS_CUDA(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(SortSmem)));
+        RS_CUDA(cudaFuncSetAttribute(k_onesweep<false, KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(SortSmem<KeyT>)));
+        RS_CUDA(cudaFuncSetAttribute(k_onesweep<true, KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(SortSmem<KeyT>)));
         attr_set = true;
     }
     long long tiles = (count + kTile - 1) / kTile;
-    u64 *kin = keys, *kout = keys_alt;
+    KeyT *kin = keys, *kout = keys_alt;
     unsigned *vin = vals, *vout = vals_alt;
     bool from_text = tk != nullptr;
     for (int p = 0; p < passes; ++p) {
@@ -251,10 +254,12 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
         if (trivial && !(from_text && p == passes - 1)) continue;  // the text must be materialised once
         Scratch s = scratch(c, tiles * kRadix);
         if (from_text)
-            RS_LAUNCH_B(c, 12.25 * count, k_onesweep<true>, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout,
+            RS_LAUNCH_B(c, (4.0 + sizeof(KeyT) + 0.25) * count, (k_onesweep<true, KeyT>), (unsigned)tiles, kNT,
+                        sizeof(SortSmem<KeyT>), kin, vin, kout,
                         vout, count, 8 * p, hist + (size_t)p * kRadix, s.counter, s.status, tkv);
         else
-            RS_LAUNCH_B(c, 24.0 * count, k_onesweep<false>, (unsigned)tiles, kNT, sizeof(SortSmem), kin, vin, kout,
+            RS_LAUNCH_B(c, 2.0 * (4.0 + sizeof(KeyT)) * count, (k_onesweep<false, KeyT>), (unsigned)tiles, kNT,
+                        sizeof(SortSmem<KeyT>), kin, vin, kout,
                         vout, count, 8 * p, hist + (size_t)p * kRadix, s.counter, s.status, tkv);
         from_text = false;
         std::swap(kin, kout);
@@ -263,5 +268,10 @@ void radix_sort_pairs(rs_ctx *c, u64 *keys, u64 *keys_alt, unsigned *vals, unsig
     *keys_out = kin;
     *vals_out = vin;
 }
+
+template void radix_sort_pairs<unsigned>(rs_ctx *, unsigned *, unsigned *, unsigned *, unsigned *, long long, int,
+                                         unsigned **, unsigned **, const TextKeys *);
+template void radix_sort_pairs<u64>(rs_ctx *, u64 *, u64 *, unsigned *, unsigned *, long long, int, u64 **,
+                                    unsigned **, const TextKeys *);
 
 }  // namespace rsb

@@ -124,8 +124,36 @@ __device__ __forceinline__ unsigned key_lcp(u64 a, u64 b, int code_bits, int key
 // (P[t], or t itself in round 0 when P is null): sa[Pos(t)] = suffix,
 // isa[suffix] = SA slot of its new group head, and the slots still in
 // non-singleton groups are compacted into P_next.
-template <bool REDUCE>
-__global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, const unsigned *__restrict__ vals,
+template <typename KeyT>
+__device__ __forceinline__ void load_keys(const KeyT *__restrict__ keys, long long t0, long long U, u64 *k) {
+    if (t0 + kUIPT <= U) {
+        if (sizeof(KeyT) == 8) {
+            const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(keys + t0);
+#pragma unroll
+            for (int j = 0; j < kUIPT / 2; ++j) {
+                ulonglong2 q = p[j];
+                k[2 * j] = q.x;
+                k[2 * j + 1] = q.y;
+            }
+        } else {
+            const uint4 *p = reinterpret_cast<const uint4 *>(keys + t0);
+#pragma unroll
+            for (int j = 0; j < kUIPT / 4; ++j) {
+                uint4 q = p[j];
+                k[4 * j] = q.x;
+                k[4 * j + 1] = q.y;
+                k[4 * j + 2] = q.z;
+                k[4 * j + 3] = q.w;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kUIPT; ++j) k[j] = (t0 + j < U) ? (u64)keys[t0 + j] : ~0ull;
+    }
+}
+
+template <bool REDUCE, typename KeyT>
+__global__ void __launch_bounds__(kUNT) k_update(const KeyT *__restrict__ keys, const unsigned *__restrict__ vals,
                                                  const unsigned *__restrict__ P, long long U,
                                                  unsigned *__restrict__ sa, unsigned *__restrict__ isa,
                                                  unsigned *__restrict__ P_next, unsigned *__restrict__ H_next,
@@ -145,22 +173,11 @@ __global__ void __launch_bounds__(kUNT) k_update(const u64 *__restrict__ keys, c
     const long long tile_t0 = tile * kUTile;
     const int tile_n = (int)((U - tile_t0) < kUTile ? (U - tile_t0) : kUTile);
     u64 k[kUIPT];
-    if (t0 + kUIPT <= U) {
-        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(keys + t0);
-#pragma unroll
-        for (int j = 0; j < kUIPT / 2; ++j) {
-            ulonglong2 q = p[j];
-            k[2 * j] = q.x;
-            k[2 * j + 1] = q.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < kUIPT; ++j) k[j] = (t0 + j < U) ? keys[t0 + j] : ~0ull;
-    }
+    load_keys<KeyT>(keys, t0, U, k);
     u64 kprev = __shfl_up_sync(0xffffffffu, k[kUIPT - 1], 1);
     u64 knext = __shfl_down_sync(0xffffffffu, k[0], 1);
-    if (lane == 0) kprev = (t0 > 0 && t0 - 1 < U) ? keys[t0 - 1] : 0;
-    if (lane == 31) knext = (t0 + kUIPT < U) ? keys[t0 + kUIPT] : 0;
+    if (lane == 0) kprev = (t0 > 0 && t0 - 1 < U) ? (u64)keys[t0 - 1] : 0;
+    if (lane == 31) knext = (t0 + kUIPT < U) ? (u64)keys[t0 + kUIPT] : 0;
     // round 0: a short suffix (fewer than K symbols) is never tied -- its
     // padded key may equal longer suffixes' keys, but the input order already
     // placed it correctly (k_init_keys), so it forms its own group.
@@ -491,15 +508,19 @@ void build_suffix_array(rs_ctx *c, long long n) {
     RS_LAUNCH_B(c, (double)n + 8.0 * words, k_pack_text, grid_for(words, 256), 256, 0, text, n, ct, bits, words,
                 stream);
     const TextKeys tk{stream, n, bits, K, std::min<long long>(K - 1, n)};
-    u64 *ks;
+    // round-0 keys of <= 32 bits (DNA) travel as u32: 8 instead of 12 bytes per pair and pass
+    const bool key32 = bits * K <= 32;
+    u64 *ks = nullptr;
+    unsigned *ks32 = nullptr;
     unsigned *vs;
-    radix_sort_pairs(c, k0, k1, v0, v1, n, bits * K, &ks, &vs, &tk);
+    if (key32)
+        radix_sort_pairs<unsigned>(c, (unsigned *)k0, (unsigned *)k1, v0, v1, n, bits * K, &ks32, &vs, &tk);
+    else
+        radix_sort_pairs<u64>(c, k0, k1, v0, v1, n, bits * K, &ks, &vs, &tk);
 
     long long U = n;
     const unsigned *P = nullptr;
     long long depth = K;
-    // bits of a round key hi*(n+1)+lo < n*(n+1)
-
     while (true) {
         ++c->sa_rounds;
         long long tiles = (U + kUTile - 1) / kUTile;
@@ -509,12 +530,21 @@ void build_suffix_array(rs_ctx *c, long long n) {
         if (!P) be = bucket_setup(c, n, 0, true);
         else if (U >= n / 16) be = bucket_setup(c, n, 0, false);
         // reduce-then-scan instead of a look-back: the heavy pass never waits
-        RS_LAUNCH_B(c, 8.0 * U, k_update<true>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha, Va, tagg,
-                    tpre, lcp_d, bits, bits * K, be);
-        RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
-        // round 0: 12 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
-        RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, k_update<false>, (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa,
-                    Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
+        if (ks32) {
+            RS_LAUNCH_B(c, 4.0 * U, (k_update<true, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa, Pa,
+                        Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
+            RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
+            // round 0: 8 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
+            RS_LAUNCH_B(c, 28.0 * U, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa,
+                        Pa, Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
+            ks32 = nullptr;
+        } else {
+            RS_LAUNCH_B(c, 8.0 * U, (k_update<true, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha,
+                        Va, tagg, tpre, lcp_d, bits, bits * K, be);
+            RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
+            RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa,
+                        isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
+        }
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
         add_bytes_last(c, 4.0 * (double)un);
@@ -532,7 +562,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
         // bits of a round key hi*(n+h+1)+lo < n*(n+h+1)
         int rbits = (int)std::ceil(std::log2((double)n * (double)(n + depth + 1)));
         if (rbits < 1) rbits = 1;
-        radix_sort_pairs(c, k0, k1, v0, v1, U, rbits, &ks, &vs);
+        radix_sort_pairs<u64>(c, k0, k1, v0, v1, U, rbits, &ks, &vs);
         depth *= 2;
     }
     c->lcp_from_keys = true;
