@@ -146,6 +146,13 @@ void add_bytes_last(rs_ctx *c, double bytes);
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);      \
         ::rsb::after_launch((ctx), #kernel, (double)(bytes));                  \
     } while (0)
+// Same with an explicit profile name (template instantiations with type args).
+#define RS_LAUNCH_NB(ctx, name, bytes, kernel, grid, block, smem, ...)        \
+    do {                                                                       \
+        ::rsb::before_launch(ctx);                                             \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);      \
+        ::rsb::after_launch((ctx), (name), (double)(bytes));                   \
+    } while (0)
 #define RS_LAUNCH(ctx, kernel, grid, block, smem, ...) \
     RS_LAUNCH_B(ctx, 0, kernel, grid, block, smem, __VA_ARGS__)
 

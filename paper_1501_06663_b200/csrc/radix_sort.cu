@@ -227,9 +227,10 @@ void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, uns
     RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
     unsigned hist_blocks = (unsigned)std::min<long long>((count + kNT * 16 - 1) / (kNT * 16), c->sm_count * 8);
     if (tk)
-        RS_LAUNCH_B(c, 0.25 * count, (k_histograms<true, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+        RS_LAUNCH_NB(c, "k_histograms<text>", 0.25 * count, (k_histograms<true, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
     else
-        RS_LAUNCH_B(c, (double)sizeof(KeyT) * count, (k_histograms<false, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+        RS_LAUNCH_NB(c, sizeof(KeyT) == 4 ? "k_histograms<u32>" : "k_histograms<u64>", (double)sizeof(KeyT) * count,
+                     (k_histograms<false, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
     // Host needs the histograms to skip constant-digit passes.
     std::vector<unsigned long long> h((size_t)passes * kRadix);
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
@@ -254,11 +255,13 @@ void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, uns
         if (trivial && !(from_text && p == passes - 1)) continue;  // the text must be materialised once
         Scratch s = scratch(c, tiles * kRadix);
         if (from_text)
-            RS_LAUNCH_B(c, (4.0 + sizeof(KeyT) + 0.25) * count, (k_onesweep<true, KeyT>), (unsigned)tiles, kNT,
+            RS_LAUNCH_NB(c, sizeof(KeyT) == 4 ? "k_onesweep<text,u32>" : "k_onesweep<text,u64>",
+                         (4.0 + sizeof(KeyT) + 0.25) * count, (k_onesweep<true, KeyT>), (unsigned)tiles, kNT,
                         sizeof(SortSmem<KeyT>), kin, vin, kout,
                         vout, count, 8 * p, hist + (size_t)p * kRadix, s.counter, s.status, tkv);
         else
-            RS_LAUNCH_B(c, 2.0 * (4.0 + sizeof(KeyT)) * count, (k_onesweep<false, KeyT>), (unsigned)tiles, kNT,
+            RS_LAUNCH_NB(c, sizeof(KeyT) == 4 ? "k_onesweep<u32>" : "k_onesweep<u64>",
+                         2.0 * (4.0 + sizeof(KeyT)) * count, (k_onesweep<false, KeyT>), (unsigned)tiles, kNT,
                         sizeof(SortSmem<KeyT>), kin, vin, kout,
                         vout, count, 8 * p, hist + (size_t)p * kRadix, s.counter, s.status, tkv);
         from_text = false;
