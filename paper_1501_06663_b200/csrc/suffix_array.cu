@@ -114,7 +114,9 @@ __device__ __forceinline__ unsigned key_lcp(u64 a, u64 b, int code_bits, int key
     const u64 x = a ^ b;
     const unsigned m = rem_a < rem_b ? rem_a : rem_b;
     if (x) {
-        const unsigned l = (unsigned)((__clzll((long long)x) - (64 - key_bits)) / code_bits);
+        const unsigned z = (unsigned)(__clzll((long long)x) - (64 - key_bits));
+        // code_bits is 2 for DNA: avoid the integer division there
+        const unsigned l = code_bits == 2 ? z >> 1 : (code_bits == 1 ? z : z / (unsigned)code_bits);
         return l < m ? l : m;
     }
     return m < K ? m : kLcpUnknown;
@@ -153,7 +155,7 @@ __device__ __forceinline__ void load_keys(const KeyT *__restrict__ keys, long lo
 }
 
 template <bool REDUCE, typename KeyT>
-__global__ void __launch_bounds__(kUNT) k_update(const KeyT *__restrict__ keys, const unsigned *__restrict__ vals,
+__global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ keys, const unsigned *__restrict__ vals,
                                                  const unsigned *__restrict__ P, long long U,
                                                  unsigned *__restrict__ sa, unsigned *__restrict__ isa,
                                                  unsigned *__restrict__ P_next, unsigned *__restrict__ H_next,
