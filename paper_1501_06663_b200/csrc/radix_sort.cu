@@ -80,7 +80,7 @@ struct SortSmem {
 };
 
 template <bool TEXT, typename KeyT>
-__global__ void __launch_bounds__(kNT, 3) k_onesweep(const KeyT *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
+__global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3) k_onesweep(const KeyT *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
                                                   KeyT *__restrict__ keys_out, unsigned *__restrict__ vals_out,
                                                   long long count, int shift,
                                                   const unsigned long long *__restrict__ digit_base,
