@@ -108,6 +108,7 @@ struct rs_ctx {
     bool sa_device_built = false;
     bool raw_from_round0 = false;
     long long tsv_bytes = 0;
+    long long patch_slots = 0;              // tied slots of round 0 kept in B_PATCH
     bool out_ref_layout = false;            // B_OUT* hold the reference 1-based layout           // B_RAW filled during the SA build (+ LCP patch fix-up)           // SA/ISA/LCP built here (mutually consistent)             // B_LCP holds round-0 key LCPs (+ unknown marks)
     // per-kernel profiling (CUDA events around every launch while enabled)
     bool profiling = false;

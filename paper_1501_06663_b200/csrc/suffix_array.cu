@@ -385,11 +385,16 @@ __device__ __forceinline__ unsigned lcp_from_depth(const unsigned char *__restri
 // is recomputed here; a neighbouring pair that is itself still unknown is
 // computed redundantly (the same value its own thread writes), so threads
 // need no ordering.
+// slots: the SA slots of the suffixes tied after round 0 (only their pairs can
+// be unknown), or null to scan every slot.
 __global__ void k_lcp_patch(const unsigned char *__restrict__ text, const unsigned *__restrict__ sa, long long n,
-                            long long K, unsigned *__restrict__ lcp_d, unsigned *__restrict__ raw) {
+                            long long K, unsigned *__restrict__ lcp_d, unsigned *__restrict__ raw,
+                            const unsigned *__restrict__ slots, long long nslots) {
     long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x + 1; r < n; r += stride) {
-        if (lcp_d[r] != kLcpUnknown) continue;
+    const long long total = slots ? nslots : n;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x + (slots ? 0 : 1); q < total; q += stride) {
+        const long long r = slots ? (long long)slots[q] : q;
+        if (r < 1 || lcp_d[r] != kLcpUnknown) continue;
         const unsigned h = lcp_from_depth(text, sa, n, K, r);
         lcp_d[r] = h;
         unsigned lp = lcp_d[r - 1];
@@ -457,6 +462,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
     c->lcp_from_keys = false;
     c->sa_device_built = false;
     c->raw_from_round0 = false;
+    c->patch_slots = 0;
     if (n <= 0) return;
     // alphabet -> order-preserving codes 1..sigma
     unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * 256);
@@ -553,7 +559,16 @@ void build_suffix_array(rs_ctx *c, long long n) {
         if (!P) bucket_apply(c, be, isa, n, raw, 1);
         else if (be.stage) bucket_apply(c, be, isa, U);
         U = (long long)un;
-        if (c->sa_rounds == 1) c->sa_unsorted_after_round0 = U;
+        if (c->sa_rounds == 1) {
+            c->sa_unsorted_after_round0 = U;
+            // keep the tied slots of round 0: the LCP patch visits only them
+            c->patch_slots = 0;
+            if (U > 0 && U <= n / 4) {
+                unsigned *keep = (unsigned *)buf(c, B_PATCH, sizeof(unsigned) * (size_t)U);
+                RS_CUDA(cudaMemcpyAsync(keep, Pa, sizeof(unsigned) * (size_t)U, cudaMemcpyDeviceToDevice, c->stream));
+                c->patch_slots = U;
+            }
+        }
         if (U == 0) break;
         if (depth >= n) fail(RS_ECUDA, "suffix sort did not converge");
         std::swap(Pa, Pb);  // Pb/Hb/Vb now hold the unsorted slots, heads, suffixes
@@ -584,9 +599,12 @@ void build_lcp(rs_ctx *c, long long n) {
     // compares; take it when that is cheaper than a full Kasai pass.
     double patch_work = (double)c->sa_unsorted_after_round0 * (1.0 + (double)c->sa_final_depth / 8.0);
     if (c->lcp_from_keys && patch_work <= 2.0 * (double)n) {
-        unsigned blocks = (unsigned)std::min<long long>(grid_for(n, 256), (long long)c->sm_count * 16);
-        RS_LAUNCH_B(c, 4.0 * n, k_lcp_patch, blocks, 256, 0, text, sa, n, (long long)c->sa_key_symbols, lcp_d,
-                    (unsigned *)c->bufs[B_RAW].p);
+        const bool list = c->patch_slots > 0;
+        const long long work = list ? c->patch_slots : n;
+        unsigned blocks = (unsigned)std::min<long long>(grid_for(work, 256), (long long)c->sm_count * 16);
+        RS_LAUNCH_B(c, list ? 8.0 * work : 4.0 * n, k_lcp_patch, blocks, 256, 0, text, sa, n,
+                    (long long)c->sa_key_symbols, lcp_d, (unsigned *)c->bufs[B_RAW].p,
+                    list ? (const unsigned *)c->bufs[B_PATCH].p : nullptr, work);
         c->raw_from_round0 = true;  // B_RAW is final
         return;
     }
