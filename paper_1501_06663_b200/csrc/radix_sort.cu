@@ -70,77 +70,87 @@ __global__ void k_materialize(TextKeys tk, long long count, KeyT *__restrict__ k
 
 template <typename KeyT>
 struct SortSmem {
-    KeyT keys[kTile];
-    unsigned vals[kTile];
+    union {
+        KeyT keys[kTile];  // keys in digit order, then
+        unsigned vals[kTile];  // values in digit order
+    } x;
     unsigned short warp_cnt[kWarps][kRadix];  // per-warp digit counts, then warp offsets
+    unsigned char digit[kTile];               // digit of each slot (value scatter)
     unsigned tile_start[kRadix];              // exclusive scan of tile digit counts
     unsigned hist[kRadix];                    // tile digit histogram
-    unsigned long long global_base[kRadix];
+    unsigned global_base[kRadix];             // < 2^32: sort counts are < 2^32 (u32 values)
     unsigned tile_id;
 };
 
+// One LSD pass over one tile of kTile pairs.  Keys first, values after (as CUB's
+// onesweep does): only keys and ranks are live in registers while ranking, the
+// value loads are issued after the key exchange and land while the keys are
+// being stored, and one shared buffer serves both exchanges.
 template <bool TEXT, typename KeyT>
-__global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3) k_onesweep(const KeyT *__restrict__ keys_in, const unsigned *__restrict__ vals_in,
-                                                  KeyT *__restrict__ keys_out, unsigned *__restrict__ vals_out,
-                                                  long long count, int shift,
-                                                  const unsigned long long *__restrict__ digit_base,
-                                                  unsigned *counter, u64 *status /*[tiles][256]*/, TextKeys tk) {
+__global__ void __launch_bounds__(kNT, (sizeof(KeyT) == 4 && !TEXT) ? 5 : 4)
+    k_onesweep(const KeyT *__restrict__ keys_in, const unsigned *__restrict__ vals_in, KeyT *__restrict__ keys_out,
+               unsigned *__restrict__ vals_out, long long count, int shift,
+               const unsigned long long *__restrict__ digit_base, unsigned *counter,
+               u64 *status /*[tiles][256]*/, TextKeys tk) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem<KeyT> &sm = *reinterpret_cast<SortSmem<KeyT> *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWarps * kRadix; i += kNT) (&sm.warp_cnt[0][0])[i] = 0;
+    {
+        unsigned *wc = reinterpret_cast<unsigned *>(&sm.warp_cnt[0][0]);
+        for (int i = threadIdx.x; i < kWarps * kRadix / 2; i += kNT) wc[i] = 0;
+    }
     sm.hist[threadIdx.x] = 0;
     if (threadIdx.x == 0) sm.tile_id = atomicAdd(counter, 1u);
     __syncthreads();
-    const long long tile = sm.tile_id;
-    const long long base = tile * kTile + (long long)warp * (kIPT * 32);
+    const unsigned tile = sm.tile_id;
+    const long long tbase = (long long)tile * kTile;
+    const int tile_count = count - tbase < kTile ? (int)(count - tbase) : kTile;
+    const int wbase = warp * (kIPT * 32) + lane;  // item i of this thread: tile offset wbase + 32 i
 
     KeyT k[kIPT];
-    unsigned v[kIPT];
-    unsigned short rank[kIPT];
+    unsigned r[kIPT];
 #pragma unroll
     for (int i = 0; i < kIPT; ++i) {
-        long long idx = base + i * 32 + lane;
-        if (idx < count) {
-            if (TEXT) {  // first pass of the round-0 sort: pairs straight from the packed text
-                const long long pos = text_pos(tk, idx);
-                k[i] = (KeyT)text_key(tk, pos);
-                v[i] = (unsigned)pos;
-            } else {
-                k[i] = keys_in[idx];
-                v[i] = vals_in[idx];
-            }
-        }
+        const int o = wbase + i * 32;
+        if (o < tile_count) k[i] = TEXT ? (KeyT)text_key(tk, text_pos(tk, tbase + o)) : keys_in[tbase + o];
     }
     // 1) tile digit histogram first, published right away (decoupled
     //    look-back: successors can use this tile's aggregate while it is still
     //    ranking, so the per-digit chains never wait on the ranking phase).
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) {
-        long long idx = base + i * 32 + lane;
-        if (idx < count) atomicAdd(&sm.hist[(unsigned)(k[i] >> shift) & 0xff], 1u);
-    }
+    for (int i = 0; i < kIPT; ++i)
+        if (wbase + i * 32 < tile_count) atomicAdd(&sm.hist[(unsigned)(k[i] >> shift) & 0xff], 1u);
     __syncthreads();
     {
         const int d = threadIdx.x;
-        const unsigned run = sm.hist[d];
-        u64 *st = status + (size_t)tile * kRadix + d;
-        st_relaxed(st, (tile == 0 ? kFlagPre : kFlagAgg) | run);
+        st_relaxed(status + (size_t)tile * kRadix + d, (tile == 0 ? kFlagPre : kFlagAgg) | sm.hist[d]);
     }
-    // 2) stable ranking within each warp (warp-striped items: item-major, lane-minor)
+    // 2) stable ranking within each warp (warp-striped items: item-major,
+    //    lane-minor): peer masks first (independent), then the short counter
+    //    chain through shared memory.  Peers come from 8 ballots (one per digit
+    //    bit): MATCH.ANY is slow when a warp holds ~30 distinct digits, which
+    //    is the common case for uniformly distributed keys.
     const unsigned lt_mask = (1u << lane) - 1;
 #pragma unroll
     for (int i = 0; i < kIPT; ++i) {
-        long long idx = base + i * 32 + lane;
-        bool valid = idx < count;
-        unsigned d = valid ? (unsigned)(k[i] >> shift) & 0xff : 0x100u;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        unsigned short before = valid ? sm.warp_cnt[warp][d & 0xff] : 0;
-        __syncwarp();
-        if (valid) {
-            rank[i] = before + (unsigned short)__popc(peers & lt_mask);
-            if ((peers & lt_mask) == 0) sm.warp_cnt[warp][d] = before + (unsigned short)__popc(peers);
+        const unsigned d = (unsigned)(k[i] >> shift) & 0xff;
+        unsigned peers = __ballot_sync(0xffffffffu, wbase + i * 32 < tile_count);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1);
+            peers &= bal ^ (((d >> b) & 1) - 1u);
         }
+        r[i] = ((unsigned)__popc(peers) << 5) | (unsigned)__popc(peers & lt_mask);
+    }
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        const bool valid = wbase + i * 32 < tile_count;
+        const unsigned d = (unsigned)(k[i] >> shift) & 0xff;
+        const unsigned before = valid ? sm.warp_cnt[warp][d] : 0;
+        __syncwarp();
+        const unsigned lt = r[i] & 31;
+        if (valid && lt == 0) sm.warp_cnt[warp][d] = (unsigned short)(before + (r[i] >> 5));
+        r[i] = before + lt;
         __syncwarp();
     }
     __syncthreads();
@@ -161,51 +171,69 @@ __global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3) k_onesweep(con
         u64 prefix = 0;
         if (tile > 0) {
             // look back 4 predecessor tiles per step (4 loads in flight)
-            long long t = tile - 1;
+            long long t = (long long)tile - 1;
             while (true) {
-                u64 s[4];
+                u64 s4[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    s[q] = (t - q >= 0) ? ld_relaxed(status + (size_t)(t - q) * kRadix + d) : kFlagPre;
+                    s4[q] = (t - q >= 0) ? ld_relaxed(status + (size_t)(t - q) * kRadix + d) : kFlagPre;
                 bool done = false;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (done) break;
-                    while ((s[q] >> 62) == 0) {
+                    while ((s4[q] >> 62) == 0) {
                         __nanosleep(20);
-                        s[q] = ld_relaxed(status + (size_t)(t - q) * kRadix + d);
+                        s4[q] = ld_relaxed(status + (size_t)(t - q) * kRadix + d);
                     }
-                    prefix += s[q] & kValMask;
-                    if ((s[q] >> 62) == 2) done = true;
+                    prefix += s4[q] & kValMask;
+                    if ((s4[q] >> 62) == 2) done = true;
                 }
                 if (done) break;
                 t -= 4;
             }
             st_relaxed(status + (size_t)tile * kRadix + d, kFlagPre | (prefix + run));
         }
-        sm.global_base[d] = digit_base[d] + prefix;
+        sm.global_base[d] = (unsigned)(digit_base[d] + prefix - excl);
     }
     __syncthreads();
-    // exchange through shared memory into digit order
+    // 4) keys into digit order (r becomes the tile slot)
 #pragma unroll
     for (int i = 0; i < kIPT; ++i) {
-        long long idx = base + i * 32 + lane;
-        if (idx < count) {
-            unsigned d = (unsigned)(k[i] >> shift) & 0xff;
-            unsigned pos = sm.tile_start[d] + sm.warp_cnt[warp][d] + rank[i];
-            sm.keys[pos] = k[i];
-            sm.vals[pos] = v[i];
+        if (wbase + i * 32 < tile_count) {
+            const unsigned d = (unsigned)(k[i] >> shift) & 0xff;
+            r[i] += sm.tile_start[d] + sm.warp_cnt[warp][d];
+            sm.x.keys[r[i]] = k[i];
+        }
+    }
+    unsigned v[kIPT];
+    if (!TEXT) {
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i)
+            if (wbase + i * 32 < tile_count) v[i] = vals_in[tbase + wbase + i * 32];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kIPT; ++q) {
+        const int j = threadIdx.x + q * kNT;
+        if (j < tile_count) {
+            const KeyT key = sm.x.keys[j];
+            const unsigned d = (unsigned)(key >> shift) & 0xff;
+            sm.digit[j] = (unsigned char)d;
+            keys_out[sm.global_base[d] + j] = key;
         }
     }
     __syncthreads();
-    long long tile_count = count - tile * kTile;
-    if (tile_count > kTile) tile_count = kTile;
-    for (int j = threadIdx.x; j < tile_count; j += kNT) {
-        KeyT key = sm.keys[j];
-        unsigned d = (unsigned)(key >> shift) & 0xff;
-        unsigned long long dst = sm.global_base[d] + (j - sm.tile_start[d]);
-        keys_out[dst] = key;
-        vals_out[dst] = sm.vals[j];
+    // 5) values through the same buffer
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        const int o = wbase + i * 32;
+        if (o < tile_count) sm.x.vals[r[i]] = TEXT ? (unsigned)text_pos(tk, tbase + o) : v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kIPT; ++q) {
+        const int j = threadIdx.x + q * kNT;
+        if (j < tile_count) vals_out[sm.global_base[sm.digit[j]] + j] = sm.x.vals[j];
     }
 }
 
