@@ -21,7 +21,7 @@ struct BucketEmit {
 // Shared memory for bucket_emit with NT threads x IPT items.
 template <int NT, int IPT>
 struct EmitSmem {
-    unsigned short cnt[8][kMaxBuckets];  // per-warp bucket counts -> warp offsets
+    unsigned cnt[kMaxBuckets];           // block bucket counts
     unsigned bstart[kMaxBuckets];        // block-local start of each bucket run
     unsigned gbase[kMaxBuckets];         // global slot reserved for the block's run
     unsigned dest[NT * IPT];             // items exchanged into bucket order
@@ -32,8 +32,9 @@ struct EmitSmem {
 
 // Phase 1, called by every thread of a 256-thread block (contains
 // __syncthreads): append this thread's IPT (dest, val[, val2]) items (dest ==
-// kNoDest: none) to their buckets.  Warp-synchronous ranking (match_any, no
-// shared-memory atomics), one global atomicAdd per (block, bucket), and an
+// kNoDest: none) to their buckets.  Order inside a bucket is free, so items are
+// ranked with one shared atomic each (no MATCH, no per-warp counter
+// chain), one global atomicAdd per (block, bucket), and an
 // exchange through shared memory so each bucket's run is written by
 // consecutive threads (coalesced) instead of one scattered store per item.
 template <int NT, int IPT>
@@ -41,34 +42,16 @@ __device__ __forceinline__ void bucket_emit(const BucketEmit &be, const unsigned
                                             EmitSmem<NT, IPT> &sm, const unsigned *val2 = nullptr) {
     static_assert(NT == 256, "one thread per bucket");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned short *wc = sm.cnt[warp];
-    for (int i = lane; i < kMaxBuckets; i += 32) wc[i] = 0;
-    __syncwarp();
-    const unsigned lt = (1u << lane) - 1;
+    sm.cnt[threadIdx.x] = 0;
+    __syncthreads();
     unsigned short rank[IPT];
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const bool valid = dest[j] != kNoDest;
-        const unsigned b = valid ? dest[j] >> be.shift : 0x100u;
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        const unsigned short before = valid ? wc[b & 0xff] : 0;
-        __syncwarp();
-        if (valid) {
-            rank[j] = before + (unsigned short)__popc(peers & lt);
-            if ((peers & lt) == 0) wc[b] = before + (unsigned short)__popc(peers);
-        }
-        __syncwarp();
-    }
+    for (int j = 0; j < IPT; ++j)
+        if (dest[j] != kNoDest) rank[j] = (unsigned short)atomicAdd(&sm.cnt[dest[j] >> be.shift], 1u);
     __syncthreads();
     {
         const int b = threadIdx.x;
-        unsigned run = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const unsigned c = sm.cnt[w][b];
-            sm.cnt[w][b] = (unsigned short)run;
-            run += c;
-        }
+        const unsigned run = sm.cnt[b];
         // block-exclusive scan of the bucket totals (bucket order)
         unsigned x = run;
 #pragma unroll
@@ -90,7 +73,7 @@ __device__ __forceinline__ void bucket_emit(const BucketEmit &be, const unsigned
     for (int j = 0; j < IPT; ++j) {
         if (dest[j] == kNoDest) continue;
         const unsigned b = dest[j] >> be.shift;
-        const unsigned p = sm.bstart[b] + wc[b] + rank[j];
+        const unsigned p = sm.bstart[b] + rank[j];
         sm.dest[p] = dest[j];
         sm.val[p] = val[j];
         if (val2) sm.val2[p] = val2[j];
