@@ -68,6 +68,21 @@ __global__ void k_materialize(TextKeys tk, long long count, KeyT *__restrict__ k
     vals[e] = (unsigned)pos;
 }
 
+// peers & (lanes whose (x & bitmask) equals mine).  Written in PTX so ptxas
+// keeps the predicate form (LOP3.P + VOTE + predicated NOT + LOP3): ~30% fewer
+// issue slots than the shift/and/compare sequence it otherwise emits
+// (tools/micro/match_bench.cu: 14.3 vs 20.6 SM-cycles per warp peer mask;
+// MATCH.ANY costs 58.6 with ~30 distinct 8-bit digits per warp).
+__device__ __forceinline__ unsigned peer_bit(unsigned peers, unsigned x, unsigned bitmask) {
+    unsigned r;
+    asm("{\n .reg .pred p;\n .reg .b32 t, m, bal;\n"
+        " and.b32 t, %1, %2;\n setp.ne.u32 p, t, 0;\n vote.sync.ballot.b32 bal, p, 0xffffffff;\n"
+        " selp.b32 m, 0xffffffff, 0, p;\n xor.b32 t, bal, m;\n not.b32 t, t;\n and.b32 %0, %3, t;\n}"
+        : "=r"(r)
+        : "r"(x), "r"(bitmask), "r"(peers));
+    return r;
+}
+
 template <typename KeyT>
 struct SortSmem {
     union {
@@ -136,10 +151,7 @@ __global__ void __launch_bounds__(kNT, (sizeof(KeyT) == 4 && !TEXT) ? 5 : 4)
         const unsigned d = (unsigned)(k[i] >> shift) & 0xff;
         unsigned peers = __ballot_sync(0xffffffffu, wbase + i * 32 < tile_count);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1);
-            peers &= bal ^ (((d >> b) & 1) - 1u);
-        }
+        for (int b = 0; b < 8; ++b) peers = peer_bit(peers, d, 1u << b);
         r[i] = ((unsigned)__popc(peers) << 5) | (unsigned)__popc(peers & lt_mask);
     }
 #pragma unroll

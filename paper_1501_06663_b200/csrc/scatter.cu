@@ -35,22 +35,23 @@ __global__ void __launch_bounds__(kApplyNT) k_bucket_apply(const uint2 *__restri
     const long long begin = chunk * (kApplyNT * kApplyIPT);
     if (begin >= count) return;
     const uint2 *src = stage + (b << shift);
+    const unsigned *src2 = stage2 + (b << shift);
     uint2 v[kApplyIPT];
+    unsigned w[kApplyIPT];
+    // every load of the chunk in flight before the first store
 #pragma unroll
     for (int j = 0; j < kApplyIPT; ++j) {
         long long i = begin + j * kApplyNT + threadIdx.x;
         v[j] = i < count ? __ldcs(src + i) : make_uint2(0xffffffffu, 0);
+        if (stage2) w[j] = i < count ? __ldcs(src2 + i) : 0u;
     }
 #pragma unroll
     for (int j = 0; j < kApplyIPT; ++j)
         if (v[j].x != 0xffffffffu) out[v[j].x] = v[j].y;
     if (stage2) {
-        const unsigned *src2 = stage2 + (b << shift);
 #pragma unroll
-        for (int j = 0; j < kApplyIPT; ++j) {
-            long long i = begin + j * kApplyNT + threadIdx.x;
-            if (i < count) out2[v[j].x + out2_shift] = __ldcs(src2 + i);
-        }
+        for (int j = 0; j < kApplyIPT; ++j)
+            if (v[j].x != 0xffffffffu) out2[v[j].x + out2_shift] = w[j];
     }
 }
 
