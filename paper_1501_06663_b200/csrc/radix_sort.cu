@@ -19,8 +19,8 @@ namespace rsb {
 namespace {
 
 constexpr int kNT = 256;
-constexpr int kIPT = 12;
-constexpr int kTile = kNT * kIPT;  // 3072 pairs per tile
+constexpr int kIPT = 16;
+constexpr int kTile = kNT * kIPT;  // 4096 pairs per tile
 constexpr int kWarps = kNT / 32;
 constexpr int kRadix = 256;
 
@@ -102,7 +102,7 @@ struct SortSmem {
 // value loads are issued after the key exchange and land while the keys are
 // being stored, and one shared buffer serves both exchanges.
 template <bool TEXT, typename KeyT>
-__global__ void __launch_bounds__(kNT, (sizeof(KeyT) == 4 && !TEXT) ? 5 : 4)
+__global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3)
     k_onesweep(const KeyT *__restrict__ keys_in, const unsigned *__restrict__ vals_in, KeyT *__restrict__ keys_out,
                unsigned *__restrict__ vals_out, long long count, int shift,
                const unsigned long long *__restrict__ digit_base, unsigned *counter,
