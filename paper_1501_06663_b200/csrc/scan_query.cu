@@ -186,29 +186,49 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
     fill_windows<RAW>(c, cnt, (int)x.tile_k0, (int)x.tile_k1, x.npos, x.s_lo, x.s_hi);
 
     // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
+    // Windows of up to 32 candidates (the common case) record their ties as a
+    // bit mask relative to the window start while finding the maximum, so the
+    // tie starts are later read by iterating set bits (nt steps) instead of
+    // re-walking the window; longer windows (repetitive text) re-walk.
     unsigned best[kPPT];
-    unsigned first[kPPT];  // start of the first tie (positions with one tie skip the re-walk)
+    unsigned tmask[kPPT];  // tie mask; 0 with best > 0 means "re-walk"
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
         const int p = threadIdx.x + j * kNT;
         best[j] = 0;
-        first[j] = 0;
+        tmask[j] = 0;
         if (p >= x.npos) continue;
         const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
         unsigned bl = 0, nt = 0, bs = 0;
+        if (wh - wl <= 32u) {
+            unsigned tm = 0, bit = 1;
 #pragma unroll 1
-        for (unsigned t = wl; t < wh; ++t) {
-            const unsigned L = c.len(t);
-            if (L > bl) {
-                bl = L;
-                bs = c.start(t);
-                nt = 1;
-            } else if (L == bl) {
-                ++nt;
+            for (unsigned t = wl; t < wh; ++t, bit <<= 1) {
+                const unsigned L = c.len(t);
+                if (L > bl) {
+                    bl = L;
+                    tm = bit;
+                } else if (L == bl) {
+                    tm |= bit;
+                }
+            }
+            nt = __popc(tm);
+            if (tm) bs = c.start(wl + __ffs(tm) - 1);
+            tmask[j] = tm;
+        } else {
+#pragma unroll 1
+            for (unsigned t = wl; t < wh; ++t) {
+                const unsigned L = c.len(t);
+                if (L > bl) {
+                    bl = L;
+                    bs = c.start(t);
+                    nt = 1;
+                } else if (L == bl) {
+                    ++nt;
+                }
             }
         }
         best[j] = bl;
-        first[j] = bs;
         if (ALL) {
             x.out0[x.slot0 + p] = bl;
             x.s_cnt[p] = bl ? nt : 0;
@@ -268,12 +288,19 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         const unsigned nt = nxt - ex;
         if (nt == 0) continue;
         long long w = (long long)(tile_base + ex);
-        if (nt == 1) {
-            if (w < x.flat_cap) x.flat[w] = first[j];
+        const unsigned wl = x.s_lo[p];
+        unsigned tm = tmask[j];
+        if (tm) {
+            do {
+                const unsigned b = __ffs(tm) - 1;
+                tm &= tm - 1;
+                if (w < x.flat_cap) x.flat[w] = c.start(wl + b);
+                ++w;
+            } while (tm);
             continue;
         }
         const unsigned bl = best[j];
-        const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
+        const unsigned wh = x.s_hi[p];
 #pragma unroll 1
         for (unsigned t = wl; t < wh; ++t) {
             if (c.len(t) == bl) {
