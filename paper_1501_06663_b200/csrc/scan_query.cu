@@ -26,7 +26,7 @@ namespace rsb {
 namespace {
 
 constexpr int kNT = 256;
-constexpr int kPPT = 8;
+constexpr int kPPT = 4;
 constexpr int kG = kNT * kPPT;           // positions per tile
 constexpr int kCapC = kG + 1024;         // staged compact entries (uint2)
 constexpr int kCapR = 2 * kG + 2048;     // staged raw values (u32)
