@@ -24,22 +24,75 @@ constexpr int kTile = kNT * kIPT;  // 4096 pairs per tile
 constexpr int kWarps = kNT / 32;
 constexpr int kRadix = 256;
 
+// hist_passes < passes: only the first hist_passes digit histograms are
+// counted here (the rest follow from k_hist_shift).
 template <bool TEXT, typename KeyT>
 __global__ void __launch_bounds__(kNT) k_histograms(const KeyT *__restrict__ keys, long long count, int passes,
                                                     unsigned long long *__restrict__ hist /*[passes][256]*/,
-                                                    TextKeys tk) {
+                                                    TextKeys tk, int hist_passes) {
     __shared__ unsigned s_hist[8][kRadix];
     for (int i = threadIdx.x; i < 8 * kRadix; i += kNT) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     long long stride = (long long)gridDim.x * kNT;
     for (long long i = blockIdx.x * (long long)kNT + threadIdx.x; i < count; i += stride) {
         u64 k = TEXT ? text_key(tk, i) : (u64)keys[i];  // histograms need no particular order
-        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
+        for (int p = 0; p < hist_passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += kNT) {
         unsigned v = (&s_hist[0][0])[i];
         if (v) atomicAdd(&hist[i], (unsigned long long)v);
+    }
+}
+
+// Digit-0 histogram straight from the packed stream when digits hold whole
+// symbols (B | 8): digit 0 of the key at i is the byte-wide window of symbols
+// [i + K - 8/B, i + K); each thread takes whole 64-bit stream words and
+// extracts every window starting in them (no per-key loads).
+template <int B>
+__global__ void __launch_bounds__(kNT) k_hist_digit0(TextKeys tk, unsigned long long *__restrict__ hist) {
+    constexpr int cpw = 64 / B, cpd = 8 / B;
+    __shared__ unsigned s_hist[kRadix];
+    s_hist[threadIdx.x] = 0;
+    __syncthreads();
+    const long long j0 = tk.K - cpd, j1 = tk.n + tk.K - cpd;  // window start symbols [j0, j1)
+    const long long w_first = j0 / cpw, w_last = (j1 - 1) / cpw;
+    const long long stride = (long long)gridDim.x * kNT;
+    for (long long w = w_first + blockIdx.x * (long long)kNT + threadIdx.x; w <= w_last; w += stride) {
+        const u64 a = tk.stream[w], b = tk.stream[w + 1];
+        const long long base = w * cpw;
+        if (base >= j0 && base + cpw <= j1) {
+#pragma unroll
+            for (int q = 0; q < cpw; ++q) {
+                const u64 x = q ? (a << (q * B)) | (b >> (64 - q * B)) : a;
+                atomicAdd(&s_hist[x >> 56], 1u);
+            }
+        } else {
+            for (int q = 0; q < cpw; ++q) {
+                const long long j = base + q;
+                if (j < j0 || j >= j1) continue;
+                const u64 x = q ? (a << (q * B)) | (b >> (64 - q * B)) : a;
+                atomicAdd(&s_hist[x >> 56], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    if (s_hist[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)s_hist[threadIdx.x]);
+}
+
+// Text keys whose 8-bit digits hold whole symbols (b | 8, 8 | b*K): digit p of
+// the key at i is digit 0 of the key at i - p*cpd (cpd = 8/b symbols per
+// digit), so hist_p = hist_0 - {digit 0 of keys at [n - p*cpd, n)} + {digit p
+// of keys at [0, p*cpd)}: one counted histogram instead of `passes`.
+__global__ void k_hist_shift(unsigned long long *hist, int passes, int cpd, TextKeys tk) {
+    const int d = threadIdx.x;  // one thread per bin
+    const long long n = tk.n;
+    for (int p = 1; p < passes; ++p) {
+        long long v = (long long)hist[d];
+        const long long s = (long long)p * cpd;
+        for (long long i = n - s; i < n; ++i) v -= (long long)((text_key(tk, i) & 0xff) == (u64)d);
+        for (long long i = 0; i < s; ++i) v += (long long)(((text_key(tk, i) >> (8 * p)) & 0xff) == (u64)d);
+        hist[(size_t)p * kRadix + d] = (unsigned long long)v;
     }
 }
 
@@ -266,11 +319,25 @@ void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, uns
     unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * kRadix);
     RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
     unsigned hist_blocks = (unsigned)std::min<long long>((count + kNT * 16 - 1) / (kNT * 16), c->sm_count * 8);
-    if (tk)
-        RS_LAUNCH_NB(c, "k_histograms<text>", 0.25 * count, (k_histograms<true, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+    // symbol-aligned text digits: count digit 0 only, shift the rest
+    const bool shifted = tk && (8 % tkv.b) == 0 && (tkv.b * tkv.K) % 8 == 0 && tkv.b * tkv.K == bits &&
+                         count == tkv.n && count > (long long)passes * (8 / tkv.b);
+    if (shifted) {
+        const long long words = (count * tkv.b + 63) / 64;
+        const unsigned hb = (unsigned)std::max<long long>(1, std::min<long long>((words + kNT - 1) / kNT, c->sm_count * 8));
+        switch (tkv.b) {
+            case 1: RS_LAUNCH_NB(c, "k_hist_digit0", count / 8.0, k_hist_digit0<1>, hb, kNT, 0, tkv, hist); break;
+            case 2: RS_LAUNCH_NB(c, "k_hist_digit0", count / 4.0, k_hist_digit0<2>, hb, kNT, 0, tkv, hist); break;
+            case 4: RS_LAUNCH_NB(c, "k_hist_digit0", count / 2.0, k_hist_digit0<4>, hb, kNT, 0, tkv, hist); break;
+            default: RS_LAUNCH_NB(c, "k_hist_digit0", 1.0 * count, k_hist_digit0<8>, hb, kNT, 0, tkv, hist); break;
+        }
+    } else if (tk)
+        RS_LAUNCH_NB(c, "k_histograms<text>", 0.25 * count, (k_histograms<true, KeyT>), hist_blocks, kNT, 0, keys, count,
+                     passes, hist, tkv, passes);
     else
         RS_LAUNCH_NB(c, sizeof(KeyT) == 4 ? "k_histograms<u32>" : "k_histograms<u64>", (double)sizeof(KeyT) * count,
-                     (k_histograms<false, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv);
+                     (k_histograms<false, KeyT>), hist_blocks, kNT, 0, keys, count, passes, hist, tkv, passes);
+    if (shifted && passes > 1) RS_LAUNCH(c, k_hist_shift, 1, kRadix, 0, hist, passes, 8 / tkv.b, tkv);
     // Host needs the histograms to skip constant-digit passes.
     std::vector<unsigned long long> h((size_t)passes * kRadix);
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());

@@ -55,29 +55,65 @@ __device__ __forceinline__ u64 load8(const unsigned char *t, long long p) {
     return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
 }
 
-__global__ void k_byte_hist(const unsigned char *__restrict__ text, long long n,
-                            unsigned long long *__restrict__ hist) {
-    __shared__ unsigned s[256];
-    s[threadIdx.x] = 0;
+// Which byte values occur (the code table needs presence only): 16-byte
+// loads and one shared byte flag store per text byte (benign same-value
+// races, no atomics), then one global atomicOr per present value and block.
+__global__ void k_byte_present(const unsigned char *__restrict__ text, long long n, unsigned *__restrict__ present) {
+    __shared__ unsigned s_flag[64];  // 256 byte flags
+    if (threadIdx.x < 64) s_flag[threadIdx.x] = 0;
     __syncthreads();
-    long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-        atomicAdd(&s[text[i]], 1u);
+    unsigned char *flag = reinterpret_cast<unsigned char *>(s_flag);
+    const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const bool vec = ((unsigned long long)text & 15) == 0;
+    const long long nv = vec ? n / 16 : 0;
+    const uint4 *tv = reinterpret_cast<const uint4 *>(text);
+    for (long long v = gid; v < nv; v += stride) {
+        const uint4 q = tv[v];
+        const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) flag[(w[k] >> (8 * j)) & 0xff] = 1;
+    }
+    for (long long i = nv * 16 + gid; i < n; i += stride) flag[text[i]] = 1;
     __syncthreads();
-    if (s[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)s[threadIdx.x]);
+    if (threadIdx.x < 256 && flag[threadIdx.x]) atomicOr(&present[threadIdx.x >> 5], 1u << (threadIdx.x & 31));
 }
 
 // Text -> big-endian bit stream of b-bit codes (one 64-bit word per thread),
-// zero padded past the end.
+// zero padded past the end.  Code table in shared memory (a table indexed by
+// data in the parameter/constant space serialises divergent lanes); for
+// b in {1, 2, 4, 8} a word covers whole 16-byte (8-byte) vectors of text.
 __global__ void k_pack_text(const unsigned char *__restrict__ text, long long n, CodeTable ct, int b,
                             long long words, u64 *__restrict__ stream) {
+    __shared__ unsigned char s_code[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_code[i] = (unsigned char)ct.code[i];
+    __syncthreads();
     long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (w >= words) return;
     const long long bit0 = w * 64;
-    long long p = bit0 / b;
+    const int cpw = 64 / b;  // codes per word when b divides 64
+    const bool fast = (64 % b) == 0 && cpw >= 8 && ((unsigned long long)text & 15) == 0 &&
+                      (w + 1) * (long long)cpw <= n;
     u64 x = 0;
+    if (fast) {
+        const unsigned char *src = text + w * (long long)cpw;
+        int j = 0;
+        for (int v = 0; v < cpw; v += 8) {  // 8 bytes per step (16-byte vectors pair up)
+            const uint2 q = *reinterpret_cast<const uint2 *>(src + v);
+#pragma unroll
+            for (int k = 0; k < 8; ++k, ++j) {
+                const unsigned byte = ((k < 4 ? q.x : q.y) >> (8 * (k & 3))) & 0xff;
+                x |= (u64)s_code[byte] << (64 - b * (j + 1));
+            }
+        }
+        stream[w] = x;
+        return;
+    }
+    long long p = bit0 / b;
     for (; p * b < bit0 + 64; ++p) {
-        const u64 code = p < n ? ct.code[text[p]] : 0;
+        const u64 code = p < n ? s_code[text[p]] : 0;
         const long long off = p * b - bit0;  // bit offset of this code's MSB within the word (may be < 0)
         const int sh = 64 - b - (int)off;     // left shift placing the code
         if (sh >= 0) x |= code << sh;
@@ -464,18 +500,18 @@ void build_suffix_array(rs_ctx *c, long long n) {
     c->raw_from_round0 = false;
     c->patch_slots = 0;
     if (n <= 0) return;
-    // alphabet -> order-preserving codes 1..sigma
-    unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * 256);
-    RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 256, c->stream));
-    unsigned hb = (unsigned)std::min<long long>((n + 256 * 64 - 1) / (256 * 64), c->sm_count * 4);
-    RS_LAUNCH_B(c, 1.0 * n, k_byte_hist, hb, 256, 0, text, n, hist);
-    std::vector<unsigned long long> h(256);
-    fetch_small(c, h.data(), hist, sizeof(unsigned long long) * 256);
+    // alphabet -> order-preserving codes 0..sigma-1 (presence of each byte value)
+    unsigned *present = (unsigned *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * 256);
+    RS_CUDA(cudaMemsetAsync(present, 0, sizeof(unsigned) * 8, c->stream));
+    unsigned hb = (unsigned)std::min<long long>((n + 256 * 64 - 1) / (256 * 64), c->sm_count * 8);
+    RS_LAUNCH_B(c, 1.0 * n, k_byte_present, hb, 256, 0, text, n, present);
+    unsigned pres[8];
+    fetch_small(c, pres, present, sizeof(pres));
     CodeTable ct;
     int sigma = 0;
     // order-preserving codes 0..sigma-1; past the end pads with code 0 too
     // (ties this creates are broken by suffix length in the next rounds)
-    for (int b = 0; b < 256; ++b) ct.code[b] = h[b] ? (unsigned short)(sigma++) : 0;
+    for (int b = 0; b < 256; ++b) ct.code[b] = (pres[b >> 5] >> (b & 31) & 1) ? (unsigned short)(sigma++) : 0;
     int bits = 1;
     while ((1 << bits) < sigma) ++bits;
     // Round-0 key length: all Kmax symbols that fit in 64 bits, unless fewer
