@@ -190,6 +190,7 @@ void invalidate(rs_ctx *c) {
     c->have_text = c->have_sa = c->have_lcp = c->have_raw = c->have_compact = false;
     c->sa_device_built = false;
     c->raw_from_round0 = false;
+    c->packed_bits = 0;
     c->out_mode = -1;
     c->n = -1;
 }

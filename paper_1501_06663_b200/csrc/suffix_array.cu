@@ -397,23 +397,42 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const u64 *__restrict__ agg,
     if (threadIdx.x == 1023) *U_next = s_w[31] & ((1ull << 31) - 1);
 }
 
-// LCP of the adjacent suffixes at SA slots r-1, r, known to be >= K.
-__device__ __forceinline__ unsigned lcp_from_depth(const unsigned char *__restrict__ text,
-                                                   const unsigned *__restrict__ sa, long long n, long long K,
-                                                   long long r) {
-    long long a = sa[r - 1], b = sa[r];
-    long long lim = n - (a > b ? a : b);
-    long long h = K < lim ? K : lim;
+// 64 bits of the packed symbol stream starting at symbol p.
+__device__ __forceinline__ u64 load_sym64(const u64 *__restrict__ stream, int b, long long p) {
+    const long long o = (long long)b * p;
+    const u64 *w = stream + (o >> 6);
+    const unsigned sh = (unsigned)(o & 63);
+    const u64 lo = __ldg(w);
+    return sh ? (lo << sh) | (__ldg(w + 1) >> (64 - sh)) : lo;
+}
+
+// Common prefix length of the suffixes at i and j, starting the comparison at
+// offset h0 and capped by lim = n - max(i, j).  Compares 64 / b symbols per
+// step on the packed stream (code equality == byte equality; the stream is
+// L2-resident at 256 Mi DNA), instead of 8 bytes of the raw text.
+__device__ __forceinline__ long long packed_lcp(const u64 *__restrict__ stream, int b, long long i, long long j,
+                                                long long h0, long long lim) {
+    long long h = h0;
+    const int per = 64 / b;
     while (h < lim) {
-        u64 x = load8(text, a + h) ^ load8(text, b + h);
+        const u64 x = load_sym64(stream, b, i + h) ^ load_sym64(stream, b, j + h);
         if (x == 0) {
-            h += 8;
+            h += per;
         } else {
-            h += (__ffsll((long long)x) - 1) >> 3;
+            h += __clzll((long long)x) / b;
             break;
         }
     }
-    return (unsigned)(h > lim ? lim : h);
+    return h > lim ? lim : h;
+}
+
+// LCP of the adjacent suffixes at SA slots r-1, r, known to be >= K.
+__device__ __forceinline__ unsigned lcp_from_depth(const u64 *__restrict__ stream, int b,
+                                                   const unsigned *__restrict__ sa, long long n, long long K,
+                                                   long long r) {
+    const long long a = sa[r - 1], c = sa[r];
+    const long long lim = n - (a > c ? a : c);
+    return (unsigned)packed_lcp(stream, b, a, c, K < lim ? K : lim, lim);
 }
 
 // Adjacent pairs whose round-0 keys were equal: lcp >= K, finished by 8-byte
@@ -423,7 +442,7 @@ __device__ __forceinline__ unsigned lcp_from_depth(const unsigned char *__restri
 // need no ordering.
 // slots: the SA slots of the suffixes tied after round 0 (only their pairs can
 // be unknown), or null to scan every slot.
-__global__ void k_lcp_patch(const unsigned char *__restrict__ text, const unsigned *__restrict__ sa, long long n,
+__global__ void k_lcp_patch(const u64 *__restrict__ stream, int b, const unsigned *__restrict__ sa, long long n,
                             long long K, unsigned *__restrict__ lcp_d, unsigned *__restrict__ raw,
                             const unsigned *__restrict__ slots, long long nslots) {
     long long stride = (long long)gridDim.x * blockDim.x;
@@ -431,12 +450,12 @@ __global__ void k_lcp_patch(const unsigned char *__restrict__ text, const unsign
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x + (slots ? 0 : 1); q < total; q += stride) {
         const long long r = slots ? (long long)slots[q] : q;
         if (r < 1 || lcp_d[r] != kLcpUnknown) continue;
-        const unsigned h = lcp_from_depth(text, sa, n, K, r);
+        const unsigned h = lcp_from_depth(stream, b, sa, n, K, r);
         lcp_d[r] = h;
         unsigned lp = lcp_d[r - 1];
-        if (lp == kLcpUnknown) lp = lcp_from_depth(text, sa, n, K, r - 1);
+        if (lp == kLcpUnknown) lp = lcp_from_depth(stream, b, sa, n, K, r - 1);
         unsigned ln = lcp_d[r + 1];
-        if (ln == kLcpUnknown) ln = lcp_from_depth(text, sa, n, K, r + 1);
+        if (ln == kLcpUnknown) ln = lcp_from_depth(stream, b, sa, n, K, r + 1);
         raw[sa[r - 1] + 1] = lp > h ? lp : h;
         raw[sa[r] + 1] = h > ln ? h : ln;
     }
@@ -450,8 +469,8 @@ __global__ void k_phi(const unsigned *__restrict__ sa, long long n, unsigned *__
 }
 
 // Kasai over text-order chunks: PLCP[i] = lcp(i, phi[i]); carry h-1 within a chunk.
-__global__ void k_plcp(const unsigned char *__restrict__ text, const unsigned *__restrict__ phi, long long n,
-                       long long chunk, unsigned *__restrict__ plcp) {
+__global__ void k_plcp(const unsigned char *__restrict__ text, const u64 *__restrict__ stream, int b,
+                       const unsigned *__restrict__ phi, long long n, long long chunk, unsigned *__restrict__ plcp) {
     long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     long long i0 = c * chunk;
     if (i0 >= n) return;
@@ -465,13 +484,17 @@ __global__ void k_plcp(const unsigned char *__restrict__ text, const unsigned *_
             continue;
         }
         long long lim = n - (i > (long long)j ? i : (long long)j);  // min remaining length
-        while (h < lim) {
-            u64 x = load8(text, i + h) ^ load8(text, (long long)j + h);
-            if (x == 0) {
-                h += 8;
-            } else {
-                h += (__ffsll((long long)x) - 1) >> 3;
-                break;
+        if (stream) {
+            h = packed_lcp(stream, b, i, (long long)j, h, lim);
+        } else {
+            while (h < lim) {
+                u64 x = load8(text, i + h) ^ load8(text, (long long)j + h);
+                if (x == 0) {
+                    h += 8;
+                } else {
+                    h += (__ffsll((long long)x) - 1) >> 3;
+                    break;
+                }
             }
         }
         if (h > lim) h = lim;
@@ -551,6 +574,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
     u64 *stream = (u64 *)buf(c, B_PACKED, sizeof(u64) * (size_t)words);
     RS_LAUNCH_B(c, (double)n + 8.0 * words, k_pack_text, grid_for(words, 256), 256, 0, text, n, ct, bits, words,
                 stream);
+    c->packed_bits = bits;
     const TextKeys tk{stream, n, bits, K, std::min<long long>(K - 1, n)};
     // round-0 keys of <= 32 bits (DNA) travel as u32: 8 instead of 12 bytes per pair and pass
     const bool key32 = bits * K <= 32;
@@ -638,7 +662,8 @@ void build_lcp(rs_ctx *c, long long n) {
         const bool list = c->patch_slots > 0;
         const long long work = list ? c->patch_slots : n;
         unsigned blocks = (unsigned)std::min<long long>(grid_for(work, 256), (long long)c->sm_count * 16);
-        RS_LAUNCH_B(c, list ? 8.0 * work : 4.0 * n, k_lcp_patch, blocks, 256, 0, text, sa, n,
+        RS_LAUNCH_B(c, list ? 8.0 * work : 4.0 * n, k_lcp_patch, blocks, 256, 0,
+                    (const u64 *)c->bufs[B_PACKED].p, c->packed_bits, sa, n,
                     (long long)c->sa_key_symbols, lcp_d, (unsigned *)c->bufs[B_RAW].p,
                     list ? (const unsigned *)c->bufs[B_PATCH].p : nullptr, work);
         c->raw_from_round0 = true;  // B_RAW is final
@@ -650,7 +675,9 @@ void build_lcp(rs_ctx *c, long long n) {
     RS_LAUNCH_B(c, 8.0 * n, k_phi, grid_for(n, 256), 256, 0, sa, n, phi);
     long long chunk = std::max<long long>(32, n >> 19);
     long long chunks = (n + chunk - 1) / chunk;
-    RS_LAUNCH_B(c, 10.0 * n, k_plcp, grid_for(chunks, 128), 128, 0, text, phi, n, chunk, plcp);
+    const u64 *stream = c->packed_bits ? (const u64 *)c->bufs[B_PACKED].p : nullptr;
+    RS_LAUNCH_B(c, 10.0 * n, k_plcp, grid_for(chunks, 128), 128, 0, text, stream, c->packed_bits, phi, n, chunk,
+                plcp);
     RS_LAUNCH_B(c, 12.0 * n, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
 }
 
