@@ -77,6 +77,35 @@ __global__ void __launch_bounds__(kRNT) k_raw_sa_emit(const unsigned *__restrict
     bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
 }
 
+// phi[sa[j]] = sa[j-1] (kNone at j = 0), emitted in SA order.
+__global__ void __launch_bounds__(kRNT) k_phi_emit(const unsigned *__restrict__ sa, long long n, BucketEmit be) {
+    __shared__ EmitSmem<kRNT, kRIPT> sm;
+    const long long j0 = (blockIdx.x * (long long)kRNT + threadIdx.x) * kRIPT;
+    unsigned dest[kRIPT], val[kRIPT];
+#pragma unroll
+    for (int q = 0; q < kRIPT; ++q) {
+        const long long j = j0 + q;
+        dest[q] = j < n ? sa[j] : kNoDest;
+        val[q] = (j < n && j > 0) ? sa[j - 1] : 0xffffffffu;
+    }
+    bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
+}
+
+// out[dest[i]] = val[i] for i < n (dest a permutation of its range).
+__global__ void __launch_bounds__(kRNT) k_pair_emit(const unsigned *__restrict__ dest_in,
+                                                   const unsigned *__restrict__ val_in, long long n, BucketEmit be) {
+    __shared__ EmitSmem<kRNT, kRIPT> sm;
+    const long long i0 = (blockIdx.x * (long long)kRNT + threadIdx.x) * kRIPT;
+    unsigned dest[kRIPT], val[kRIPT];
+#pragma unroll
+    for (int q = 0; q < kRIPT; ++q) {
+        const long long i = i0 + q;
+        dest[q] = i < n ? dest_in[i] : kNoDest;
+        val[q] = i < n ? val_in[i] : 0u;
+    }
+    bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
+}
+
 }  // namespace
 
 BucketEmit bucket_setup(rs_ctx *c, long long n_out, int slot, bool two) {
@@ -112,6 +141,18 @@ void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n) {
     RS_LAUNCH_B(c, 16.0 * n, k_raw_sa_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0,
                 (const unsigned *)c->bufs[B_SA].p, (const unsigned *)c->bufs[B_LCP].p, n, be);
     bucket_apply(c, be, raw, n);
+}
+
+void scatter_phi(rs_ctx *c, const unsigned *sa, long long n, unsigned *phi) {
+    BucketEmit be = bucket_setup(c, n, 0);
+    RS_LAUNCH_B(c, 12.0 * n, k_phi_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0, sa, n, be);
+    bucket_apply(c, be, phi, n);
+}
+
+void scatter_by(rs_ctx *c, const unsigned *dest, const unsigned *val, long long n, unsigned *out, long long n_out) {
+    BucketEmit be = bucket_setup(c, n_out, 0);
+    RS_LAUNCH_B(c, 16.0 * n, k_pair_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0, dest, val, n, be);
+    bucket_apply(c, be, out, n);
 }
 
 }  // namespace rsb

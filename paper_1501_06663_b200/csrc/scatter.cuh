@@ -93,5 +93,9 @@ BucketEmit bucket_setup(rs_ctx *c, long long n_out, int slot = 0, bool two = fal
 void bucket_apply(rs_ctx *c, const BucketEmit &be, unsigned *out, long long elems, unsigned *out2 = nullptr,
                   int out2_shift = 0);
 void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n);
+// phi[sa[j]] = sa[j-1] (0xffffffff at j = 0) through the bucketed scatter.
+void scatter_phi(rs_ctx *c, const unsigned *sa, long long n, unsigned *phi);
+// out[dest[i]] = val[i], i < n; dest a permutation into [0, n_out).
+void scatter_by(rs_ctx *c, const unsigned *dest, const unsigned *val, long long n, unsigned *out, long long n_out);
 
 }  // namespace rsb

@@ -672,13 +672,25 @@ void build_lcp(rs_ctx *c, long long n) {
     c->raw_from_round0 = false;
     unsigned *phi = (unsigned *)buf(c, B_PHI, sizeof(unsigned) * (size_t)n);
     unsigned *plcp = (unsigned *)buf(c, B_PLCP, sizeof(unsigned) * (size_t)n);
-    RS_LAUNCH_B(c, 8.0 * n, k_phi, grid_for(n, 256), 256, 0, sa, n, phi);
+    // Device-built structures: the two permutation steps (phi by SA order,
+    // PLCP -> SA order by ISA) go through the bucketed L2-local scatter
+    // instead of one random 4-byte store/load per suffix.
+    const bool bucketed = c->sa_device_built;
+    if (bucketed)
+        scatter_phi(c, sa, n, phi);
+    else
+        RS_LAUNCH_B(c, 8.0 * n, k_phi, grid_for(n, 256), 256, 0, sa, n, phi);
     long long chunk = std::max<long long>(32, n >> 19);
     long long chunks = (n + chunk - 1) / chunk;
     const u64 *stream = c->packed_bits ? (const u64 *)c->bufs[B_PACKED].p : nullptr;
     RS_LAUNCH_B(c, 10.0 * n, k_plcp, grid_for(chunks, 128), 128, 0, text, stream, c->packed_bits, phi, n, chunk,
                 plcp);
-    RS_LAUNCH_B(c, 12.0 * n, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
+    if (bucketed) {
+        RS_CUDA(cudaMemsetAsync(lcp_d + n, 0, sizeof(unsigned) * 2, c->stream));
+        scatter_by(c, (const unsigned *)c->bufs[B_ISA].p, plcp, n, lcp_d, n);
+    } else {
+        RS_LAUNCH_B(c, 12.0 * n, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
+    }
 }
 
 }  // namespace rsb
