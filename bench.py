@@ -180,6 +180,22 @@ def run_reference(args) -> None:
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
+TRAFFIC_JSON = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+
+
+def committed_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed `ncu --set full`
+    capture of the same workload (profiles/r01/traffic.json), or None."""
+    try:
+        with open(TRAFFIC_JSON) as f:
+            rec = json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None, None
+    if not rec:
+        return None, None
+    return rec["dram_bytes_per_launch"], f"profiles/r01/{rec['report']} (dram__bytes_read.sum + dram__bytes_write.sum)"
+
+
 def roofline_of(profile: list[dict], steps: int) -> tuple[dict, list[dict]]:
     peak, src = hbm_peak()
     rows = []
@@ -195,8 +211,10 @@ def roofline_of(profile: list[dict], steps: int) -> tuple[dict, list[dict]]:
                      "frac": (gbs / peak) if gbs else None})
     rows.sort(key=lambda r: -r["ms_per_step"])
     top = rows[0]
+    traffic, tsrc = committed_traffic(top["kernel"])
     roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": top["achieved_gbs"], "peak": peak,
-            "unit": "GB/s", "frac": top["frac"], "traffic": None,
+            "unit": "GB/s", "frac": top["frac"], "traffic": traffic, "traffic_source": tsrc,
+            "algorithmic_bytes_per_launch": top["bytes_per_launch"],
             "peak_source": f"{src} hbm_gbs (MEASURED_PEAKS.json)" if src == "measured" else
             "fallback 6650 GB/s (B200_PROFILING.md)"}
     return roof, rows
