@@ -461,6 +461,149 @@ __global__ void k_lcp_patch(const u64 *__restrict__ stream, int b, const unsigne
     }
 }
 
+// ---- small tied groups after round 0 ------------------------------------
+// Suffixes whose round-0 keys are equal share their first K symbols.  On
+// i.i.d.-like text these groups have 2-3 members: sorting each one directly by
+// comparing the suffixes on the packed stream (from depth K) gives their final
+// order AND the LCPs between them, which replaces a whole doubling round
+// (keys, 64-bit radix sort, update) and the LCP patch for them.  Larger groups
+// stay in the list for the doubling rounds.
+constexpr int kSmallGroup = 8;
+
+// suffix a < suffix c, given >= K equal leading symbols; l = their LCP.  The
+// 64-bit windows are big-endian code strings, so at the first difference the
+// smaller window is the smaller suffix (no extra symbol loads).
+__device__ __forceinline__ bool suffix_less(const u64 *__restrict__ stream, int b, long long n, long long K,
+                                            unsigned a, unsigned c, unsigned &l) {
+    const long long lim = n - (long long)(a > c ? a : c);
+    long long h = K < lim ? K : lim;
+    const int per = 64 / b;
+    while (h < lim) {
+        const u64 wa = load_sym64(stream, b, (long long)a + h), wc = load_sym64(stream, b, (long long)c + h);
+        const u64 x = wa ^ wc;
+        if (x == 0) {
+            h += per;
+            continue;
+        }
+        h += __clzll((long long)x) / b;
+        if (h >= lim) break;  // first difference lies past the end of the shorter suffix
+        l = (unsigned)h;
+        return wa < wc;
+    }
+    l = (unsigned)lim;
+    return a > c;  // one is a prefix of the other: the shorter (later start) sorts first
+}
+
+// One thread per list entry (groups are runs of equal heads; a group's slots
+// are head .. head+s-1).  Each entry classifies its group by looking at most
+// kSmallGroup entries each way; the first entry of a small group sorts it.
+// keep[t] = 1 marks entries of groups left to the doubling rounds.
+__global__ void k_small_groups(const unsigned *__restrict__ H, const unsigned *__restrict__ V, long long U,
+                               const u64 *__restrict__ stream, int b, long long n, long long K,
+                               unsigned *__restrict__ sa, unsigned *__restrict__ isa, unsigned *__restrict__ lcp_d,
+                               unsigned *__restrict__ raw, unsigned *__restrict__ keep) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= U) return;
+    const unsigned head = H[t];
+    int back = 0, fwd = 0;
+    while (back < kSmallGroup && t - back - 1 >= 0 && H[t - back - 1] == head) ++back;
+    while (fwd < kSmallGroup && t + fwd + 1 < U && H[t + fwd + 1] == head) ++fwd;
+    const bool small = back + fwd + 1 <= kSmallGroup;
+    keep[t] = small ? 0u : 1u;
+    if (!small || back) return;
+    const int s = fwd + 1;
+    const unsigned lb = lcp_d[head];  // group boundaries: keys differ there, LCP known from round 0
+    if (s == 2) {
+        // round 0 left sa[head..head+1] = (x, y), isa = head for both, and
+        // raw without the (unknown) inner LCP; write only what changes
+        const unsigned x = V[t], y = V[t + 1];
+        const unsigned le = lcp_d[head + 2];
+        unsigned l;
+        const bool swap = suffix_less(stream, b, n, K, y, x, l);
+        const unsigned first = swap ? y : x, second = swap ? x : y;
+        if (swap) {
+            sa[head] = y;
+            sa[head + 1] = x;
+            isa[y] = head;
+        }
+        isa[second] = head + 1;
+        lcp_d[head + 1] = l;
+        raw[first + 1] = lb > l ? lb : l;
+        raw[second + 1] = l > le ? l : le;
+        return;
+    }
+    unsigned v[kSmallGroup];
+    unsigned lc[kSmallGroup + 1];
+    lc[0] = lb;
+    lc[s] = lcp_d[head + s];
+    for (int j = 0; j < s; ++j) v[j] = V[t + j];
+    unsigned l;
+    for (int i = 1; i < s; ++i) {  // insertion sort by suffix comparison
+        const unsigned x = v[i];
+        int j = i;
+        while (j > 0 && suffix_less(stream, b, n, K, x, v[j - 1], l)) {
+            v[j] = v[j - 1];
+            --j;
+        }
+        v[j] = x;
+    }
+    for (int j = 1; j < s; ++j) {
+        suffix_less(stream, b, n, K, v[j - 1], v[j], l);
+        lc[j] = l;
+    }
+    for (int j = 0; j < s; ++j) {
+        const unsigned slot = head + j;
+        sa[slot] = v[j];
+        isa[v[j]] = slot;
+        if (j) lcp_d[slot] = lc[j];
+        raw[v[j] + 1] = lc[j] > lc[j + 1] ? lc[j] : lc[j + 1];
+    }
+}
+
+// Order-preserving compaction of the (slot, head, suffix) lists to the kept
+// entries: block scan + decoupled look-back, one pass.
+constexpr int kKNT = 256, kKIPT = 8, kKTile = kKNT * kKIPT;
+__global__ void __launch_bounds__(kKNT) k_keep_compact(const unsigned *__restrict__ keep, const unsigned *__restrict__ P,
+                                                     const unsigned *__restrict__ H, const unsigned *__restrict__ V,
+                                                     long long U, unsigned *__restrict__ P2, unsigned *__restrict__ H2,
+                                                     unsigned *__restrict__ V2, unsigned long long *total,
+                                                     unsigned *counter, u64 *status, long long tiles) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned s_warp[kKNT / 32];
+    __shared__ u64 s_base;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const long long tile = s_tile;
+    const long long i0 = tile * kKTile + (long long)threadIdx.x * kKIPT;
+    unsigned flags = 0, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kKIPT; ++j) {
+        const bool f = i0 + j < U && keep[i0 + j];
+        flags |= (unsigned)f << j;
+        cnt += f;
+    }
+    unsigned excl;
+    const unsigned tot = block_exclusive_sum<kKNT>(cnt, excl, s_warp);
+    if (threadIdx.x < 32) {
+        const u64 base = lookback_warp(status, tile, (u64)tot, OpSum());
+        if (threadIdx.x == 0) {
+            s_base = base;
+            if (tile == tiles - 1) *total = base + tot;
+        }
+    }
+    __syncthreads();
+    u64 o = s_base + excl;
+#pragma unroll
+    for (int j = 0; j < kKIPT; ++j) {
+        if (flags >> j & 1) {
+            P2[o] = P[i0 + j];
+            H2[o] = H[i0 + j];
+            V2[o] = V[i0 + j];
+            ++o;
+        }
+    }
+}
+
 // phi[sa[j]] = sa[j-1] (kNone for j = 0)
 __global__ void k_phi(const unsigned *__restrict__ sa, long long n, unsigned *__restrict__ phi) {
     long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -619,6 +762,22 @@ void build_suffix_array(rs_ctx *c, long long n) {
         if (!P) bucket_apply(c, be, isa, n, raw, 1);
         else if (be.stage) bucket_apply(c, be, isa, U);
         U = (long long)un;
+        if (c->sa_rounds == 1 && U > 0 && U <= n / 8) {  // mostly small groups (i.i.d.-like text)
+            // small tied groups: final order + LCP + raw by direct comparison;
+            // the lists keep only the larger groups (order preserved)
+            unsigned *keep = (unsigned *)buf(c, B_T4, sizeof(unsigned) * (size_t)U);
+            RS_LAUNCH_B(c, 16.0 * U, k_small_groups, grid_for(U, 256), 256, 0, Ha, Va, U, stream, bits, n,
+                        (long long)K, sa, isa, lcp_d, raw, keep);
+            const long long ktiles = (U + kKTile - 1) / kKTile;
+            Scratch ks_ = scratch(c, ktiles);
+            RS_LAUNCH_B(c, 16.0 * U, k_keep_compact, (unsigned)ktiles, kKNT, 0, keep, Pa, Ha, Va, U, Pb, Hb, Vb, u_dev,
+                        ks_.counter, ks_.status, ktiles);
+            fetch_small(c, &un, u_dev, sizeof(un));
+            U = (long long)un;
+            std::swap(Pa, Pb);
+            std::swap(Ha, Hb);
+            std::swap(Va, Vb);
+        }
         if (c->sa_rounds == 1) {
             c->sa_unsorted_after_round0 = U;
             // keep the tied slots of round 0: the LCP patch visits only them
@@ -658,6 +817,10 @@ void build_lcp(rs_ctx *c, long long n) {
     // Patch work is at most (tied suffixes) x (final depth / 8 + 1) word
     // compares; take it when that is cheaper than a full Kasai pass.
     double patch_work = (double)c->sa_unsorted_after_round0 * (1.0 + (double)c->sa_final_depth / 8.0);
+    if (c->lcp_from_keys && c->sa_unsorted_after_round0 == 0) {  // every LCP known after round 0
+        c->raw_from_round0 = true;
+        return;
+    }
     if (c->lcp_from_keys && patch_work <= 2.0 * (double)n) {
         const bool list = c->patch_slots > 0;
         const long long work = list ? c->patch_slots : n;
