@@ -202,15 +202,20 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         unsigned bl = 0, nt = 0, bs = 0;
         if (wh - wl <= 32u) {
             unsigned tm = 0, bit = 1;
+            unsigned t = wl;
+            // two candidates per iteration (branch-free updates), then the odd one
 #pragma unroll 1
-            for (unsigned t = wl; t < wh; ++t, bit <<= 1) {
-                const unsigned L = c.len(t);
-                if (L > bl) {
-                    bl = L;
-                    tm = bit;
-                } else if (L == bl) {
-                    tm |= bit;
-                }
+            for (; t + 1 < wh; t += 2, bit <<= 2) {
+                const unsigned L0 = c.len(t), L1 = c.len(t + 1);
+                tm = L0 > bl ? bit : (L0 == bl ? tm | bit : tm);
+                bl = L0 > bl ? L0 : bl;
+                tm = L1 > bl ? bit << 1 : (L1 == bl ? tm | (bit << 1) : tm);
+                bl = L1 > bl ? L1 : bl;
+            }
+            if (t < wh) {
+                const unsigned L0 = c.len(t);
+                tm = L0 > bl ? bit : (L0 == bl ? tm | bit : tm);
+                bl = L0 > bl ? L0 : bl;
             }
             nt = __popc(tm);
             if (tm) bs = c.start(wl + __ffs(tm) - 1);
@@ -278,6 +283,8 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         }
         x.out1[x.out_off] = 0;  // offsets of the first position
     }
+    const bool cap_ok = (long long)(tile_base + block_total) <= x.flat_cap;
+    long long *const flat_tile = x.flat + tile_base;
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
         const int p = threadIdx.x + j * kNT;
@@ -287,9 +294,18 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x)
         x.out1[x.slot0 + 1 + p] = (long long)(tile_base + nxt);  // offsets[k+1] = inclusive prefix
         const unsigned nt = nxt - ex;
         if (nt == 0) continue;
-        long long w = (long long)(tile_base + ex);
         const unsigned wl = x.s_lo[p];
         unsigned tm = tmask[j];
+        if (tm && cap_ok) {  // 32-bit tile-local slots, no per-store capacity test
+            unsigned w = ex;
+            do {
+                const unsigned b = __ffs(tm) - 1;
+                tm &= tm - 1;
+                flat_tile[w++] = c.start(wl + b);
+            } while (tm);
+            continue;
+        }
+        long long w = (long long)(tile_base + ex);
         if (tm) {
             do {
                 const unsigned b = __ffs(tm) - 1;

@@ -318,3 +318,31 @@ def test_walk_stats_vs_closed_form():
         assert (st.min_steps, st.max_steps, st.avg_steps, st.positions) == (0, 0, 0.0, 0)
     with pytest.raises(ValueError):
         rb.compute_walk_stats(raw, rb.compact_llr_sequential(raw), "bogus")
+
+
+def test_small_tied_groups_vs_oracle(rng):
+    # i.i.d. DNA (few ties after round 0 -> the direct small-group sort) with
+    # planted copies: groups of 2..10 equal round-0 keys, copies at the very
+    # end (comparisons that run into the end of the text: prefix order), and
+    # copies differing only deep inside (LCP far beyond the round-0 depth).
+    for trial in range(12):
+        n = int(rng.integers(20_000, 200_000))
+        data = workloads.iid_dna(n, 100 + trial).copy()
+        L = int(rng.integers(20, 200))
+        src = int(rng.integers(0, n // 2))
+        block = data[src:src + L].copy()
+        copies = int(rng.integers(1, 10))
+        for c in range(copies):
+            dst = int(rng.integers(n // 2, n - L))
+            data[dst:dst + L] = block
+            if c % 3 == 1:  # a late mutation: tie broken deep inside
+                acgt = np.frombuffer(b"ACGT", np.uint8)
+                data[dst + L - 1] = acgt[(int(np.flatnonzero(acgt == data[dst + L - 1])[0]) + 1) % 4]
+        data[n - L:] = block  # suffix of the text equal to an earlier substring
+        want = oracle.build_suffix_structures(data)
+        s = rb.build_suffix_structures(rb.Text(data))
+        assert all(np.array_equal(a, b) for a, b in zip((s.sa, s.rank, s.lcp), want)), trial
+        wl, wo, wf = oracle.all_positions(data, mode="all", structures=want)
+        A = rb.all_positions(rb.Text(data), mode="all")
+        assert np.array_equal(A.lengths, wl) and np.array_equal(A.offsets, wo), trial
+        assert np.array_equal(A.flat_starts, wf), trial
