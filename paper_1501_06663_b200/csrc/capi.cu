@@ -28,7 +28,7 @@ bool verify_structures(rs_ctx *c, const unsigned char *d_text, long long n, cons
 long long serialize_tsv(rs_ctx *c, int mode, long long lo, long long hi);
 void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned long long *acc_host);
 void summarize(rs_ctx *c, const long long *d_steps, long long count, unsigned long long *acc_host);
-void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
+bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
                  long long kb, long long ke, int out_off, long long n_slots);
 
 void fail(int code, const std::string &msg) { throw RsError{code, msg}; }
@@ -618,9 +618,21 @@ int rs_query(rs_ctx *c, int mode, int path, int64_t *total) {
         if (c->n < 0) fail(RS_ESTATE, "nothing loaded");
         long long n = c->n;
         bool used[RS_NUM_STAGES] = {};
-        if (path == RS_PATH_RAW) ensure_raw(c, used);
+        // compact path: unless LLRc already exists, compact inside the scan
+        // tiles (k_query_fused); materialise LLRc only for long repeats
+        bool fused = path == RS_PATH_COMPACT && !c->have_compact && n > 0;
+        if (path == RS_PATH_RAW || fused) ensure_raw(c, used);
         else ensure_compact(c, used);
-        {
+        if (fused) {
+            Stage st(c, RS_STAGE_QUERY);
+            used[RS_STAGE_QUERY] = true;
+            c->out_ref_layout = true;
+            if (!query_range(c, mode, path, nullptr, 0, (const unsigned *)c->bufs[B_RAW].p, 1, n, 1, n)) {
+                fused = false;
+                ensure_compact(c, used);
+            }
+        }
+        if (!fused) {
             Stage st(c, RS_STAGE_QUERY);
             used[RS_STAGE_QUERY] = true;
             if (n == 0) {

@@ -408,6 +408,113 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     }
 }
 
+// Compact path with the compaction fused into the scan.  A tile's compact
+// candidates are exactly the flagged raw slots i in [lo, klast] (flag(i) =
+// raw[i] > 0 && raw[i] >= raw[i-1]; lo = first i whose raw end reaches the
+// tile, from k_bounds<true>): flagged slots before lo end before the tile,
+// every flagged slot from lo on reaches it (raw ends are nondecreasing).  So
+// the tile stages raw[lo-1, klast] with one TMA copy, compacts it in shared
+// memory (block scan, order kept) and runs the compact walk on that list --
+// the global LLRc is never written nor read back.  The host only takes this
+// path when every tile's raw range fits the stage (short repeats).
+constexpr int kFStage = kG + 1024 + 16;  // staged raw values incl. alignment slack and slot lo-1
+constexpr int kFRawBytes = ((4 * kFStage + 127) / 128) * 128;
+constexpr int kFusedSmem = kFRawBytes + 8 * kFStage + 3 * 4 * kG;
+
+template <bool ALL>
+__global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict__ raw, long long kb, long long ke,
+                                                     const long long *__restrict__ bounds, int out_off,
+                                                     long long *__restrict__ out0, long long *__restrict__ out1,
+                                                     long long *__restrict__ flat, long long flat_cap,
+                                                     unsigned *counter, u64 *status, long long tiles,
+                                                     unsigned long long *total_out) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    unsigned *s_raw = reinterpret_cast<unsigned *>(dsm);
+    uint2 *s_list = reinterpret_cast<uint2 *>(dsm + kFRawBytes);
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ unsigned s_tile;
+    __shared__ unsigned s_warp[kNT / 32];
+    __shared__ u64 s_base;
+
+    long long tile;
+    if (ALL) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+        __syncthreads();
+        tile = s_tile;
+    } else {
+        tile = blockIdx.x;
+    }
+    TileCtx x;
+    x.tile = tile;
+    const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];  // raw slots [lo, hi)
+    x.tile_k0 = kb + tile * kG;
+    x.npos = (int)((ke - x.tile_k0 + 1) < kG ? (ke - x.tile_k0 + 1) : kG);
+    x.tile_k1 = x.tile_k0 + x.npos - 1;
+    x.slot0 = x.tile_k0 - kb + out_off;
+    x.out_off = out_off;
+    x.tiles = tiles;
+    x.flat_cap = flat_cap;
+    x.s_lo = reinterpret_cast<unsigned *>(dsm + kFRawBytes + 8 * kFStage);
+    x.s_hi = x.s_lo + kG;
+    x.s_cnt = x.s_hi + kG;
+    x.s_warp = s_warp;
+    x.s_base = &s_base;
+    x.out0 = out0;
+    x.out1 = out1;
+    x.flat = flat;
+    x.status = status;
+    x.total_out = total_out;
+
+    const long long a = (lo - 1) & ~3ll, b = (hi + 3) & ~3ll;  // stage raw[a, b), 16-byte aligned
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        const unsigned bytes = (unsigned)((b - a) * 4);
+        mbar_expect_tx(&s_bar, bytes);
+        tma_load_1d(s_raw, raw + a, bytes, &s_bar);
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+    // tile-local compaction: thread-contiguous runs, block scan, order kept
+    const int nr = (int)(hi - lo);
+    const int per = (nr + kNT - 1) / kNT;
+    const int o0 = threadIdx.x * per;
+    const unsigned *r0 = s_raw + (lo - a);  // r0[o] = raw[lo + o], r0[-1] = raw[lo - 1]
+    unsigned nf = 0;
+    for (int q = 0; q < per; ++q) {
+        const int o = o0 + q;
+        if (o < nr) nf += (r0[o] > 0u && r0[o] >= r0[o - 1]);
+    }
+    unsigned w;
+    const unsigned cnt = block_exclusive_sum<kNT>(nf, w, s_warp);
+    for (int q = 0; q < per; ++q) {
+        const int o = o0 + q;
+        if (o < nr && r0[o] > 0u && r0[o] >= r0[o - 1]) s_list[w++] = make_uint2((unsigned)(lo + o), r0[o]);
+    }
+    x.cnt = cnt;
+    for (int i = threadIdx.x; i < x.npos; i += kNT) {
+        x.s_lo[i] = cnt;
+        x.s_hi[i] = 0;
+    }
+    __syncthreads();
+    Cand<false> c;
+    c.e = s_list;
+    c.r = nullptr;
+    c.base = 0;
+    query_tile<false, ALL>(c, x);
+}
+
+// max over tiles of the staged raw range (hi - lo + 8) -> *out
+__global__ void k_max_span(const long long *__restrict__ bounds, long long tiles, unsigned long long *out) {
+    long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    unsigned long long v = 0;
+    if (t < tiles) v = (unsigned long long)(bounds[2 * t + 1] - bounds[2 * t] + 8);
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = v > y ? v : y;
+    }
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
 // Walk-step statistics (stats.py:30-76): the steps of a query walk at k are
 // exactly the candidates covering k, i.e. the window size hi(k) - lo(k)
 // (raw: k - #{i : i + raw[i] - 1 < k}; compact: max(upto - below, 0)).
@@ -505,18 +612,34 @@ __global__ void k_summarize(const long long *__restrict__ steps, long long n, un
 
 // Run the scan for positions [kb, ke] over candidates (compact entries or raw),
 // writing into B_OUT0/B_OUT1/B_FLAT.  out_off: 1 = reference layout.
-void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
+bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
                  long long kb, long long ke, int out_off, long long n_slots) {
     const bool all = mode == RS_MODE_ALL;
+    // compact path without a materialised LLRc: compaction fused into the scan
+    const bool fused = path == RS_PATH_COMPACT && d_e == nullptr;
     const bool rawp = path == RS_PATH_RAW;
     long long npos = ke - kb + 1;
-    if (npos <= 0) return;
+    if (npos <= 0) return true;
     long long tiles = (npos + kG - 1) / kG;
     long long *bounds = (long long *)buf(c, B_BOUNDS, sizeof(long long) * 2 * (size_t)tiles);
-    if (rawp)
+    if (rawp || fused)
         RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds);
     else
         RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds);
+    if (fused) {
+        unsigned long long *span = (unsigned long long *)buf(c, B_SMALL, 4096) + 6;
+        RS_CUDA(cudaMemsetAsync(span, 0, sizeof(*span), c->stream));
+        RS_LAUNCH(c, k_max_span, grid_for(tiles, 256), 256, 0, bounds, tiles, span);
+        unsigned long long mx = 0;
+        fetch_small(c, &mx, span, sizeof(mx));
+        if (mx > (unsigned long long)kFStage) return false;  // long repeats: the caller materialises LLRc
+        static bool fattr = false;
+        if (!fattr) {
+            RS_CUDA(cudaFuncSetAttribute(k_query_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+            RS_CUDA(cudaFuncSetAttribute(k_query_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+            fattr = true;
+        }
+    }
 
     static bool attr = false;
     if (!attr) {
@@ -531,17 +654,20 @@ void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     unsigned long long *tot = (unsigned long long *)buf(c, B_SMALL, 4096) + 2;
     // algorithmic bytes: candidates read once (compact 8 B/entry, raw 4 B/slot),
     // int64 outputs written once (leftmost 16 B/pos; all 16 B/pos + 8 B/tie).
-    const double cand_bytes = rawp ? 4.0 * (double)npos : 8.0 * (double)count;
+    const double cand_bytes = (rawp || fused) ? 4.0 * (double)npos : 8.0 * (double)count;
     const double qbytes = cand_bytes + 16.0 * (double)npos;
     if (!all) {
-        if (rawp)
+        if (fused)
+            RS_LAUNCH_B(c, qbytes, (k_query_fused<false>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
+                        out_off, out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
+        else if (rawp)
             RS_LAUNCH_B(c, qbytes, (k_query<true, false>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,
                       out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
         else
             RS_LAUNCH_B(c, qbytes, (k_query<false, false>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds,
                       out_off, out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
         c->out_mode = 0;
-        return;
+        return true;
     }
     // Tie total is unknown before the scan: size flat for the worst case seen
     // so far and re-run if it overflows (T <= sum of window sizes; in practice
@@ -552,7 +678,10 @@ void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     for (int attempt = 0; attempt < 3; ++attempt) {
         long long *flat = (long long *)buf(c, B_FLAT, sizeof(long long) * cap_slots);
         Scratch s = scratch(c, tiles);
-        if (rawp)
+        if (fused)
+            RS_LAUNCH_B(c, qbytes, (k_query_fused<true>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
+                        out_off, out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot);
+        else if (rawp)
             RS_LAUNCH_B(c, qbytes, (k_query<true, true>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,
                       out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot);
         else
@@ -563,7 +692,7 @@ void query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
         add_bytes_last(c, 8.0 * (double)T);
         c->total = (long long)T;
         c->out_mode = 1;
-        if ((size_t)T <= cap_slots) return;
+        if ((size_t)T <= cap_slots) return true;
         cap_slots = (size_t)T + 64;
     }
     fail(RS_ECUDA, "tie buffer sizing did not converge");
