@@ -28,6 +28,7 @@ bool verify_structures(rs_ctx *c, const unsigned char *d_text, long long n, cons
 long long serialize_tsv(rs_ctx *c, int mode, long long lo, long long hi);
 void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned long long *acc_host);
 void summarize(rs_ctx *c, const long long *d_steps, long long count, unsigned long long *acc_host);
+void ensure_isa(rs_ctx *c);
 bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
                  long long kb, long long ke, int out_off, long long n_slots);
 
@@ -191,6 +192,7 @@ void invalidate(rs_ctx *c) {
     c->sa_device_built = false;
     c->raw_from_round0 = false;
     c->packed_bits = 0;
+    c->isa_lazy = false;
     c->out_mode = -1;
     c->n = -1;
 }
@@ -586,6 +588,7 @@ int rs_get_structures(rs_ctx *c, int64_t *sa, int64_t *rank, int64_t *lcp) {
         widen_u32_to_i64(c, (const unsigned *)c->bufs[B_SA].p, dtmp + 1, n, 1);
         d2h(c, sa, dtmp, 8 * (size_t)(n + 1));
         RS_CUDA(cudaStreamSynchronize(c->stream));
+        ensure_isa(c);
         widen_u32_to_i64(c, (const unsigned *)c->bufs[B_ISA].p, dtmp + 1, n, 1);
         d2h(c, rank, dtmp, 8 * (size_t)(n + 1));
         RS_CUDA(cudaStreamSynchronize(c->stream));

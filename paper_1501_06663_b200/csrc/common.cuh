@@ -103,6 +103,7 @@ struct rs_ctx {
     long long shard_lo = 0, shard_hi = 0;
     int sa_key_symbols = 0;                 // K of the round-0 keys
     int packed_bits = 0;                    // B_PACKED holds the current text at this many bits/symbol (0: none)
+    bool isa_lazy = false;                  // B_ISA not built (device SA without later rounds): fill from SA on demand
     long long sa_unsorted_after_round0 = 0; // suffixes left in tied groups by round 0
     long long sa_final_depth = 0;          // sorted depth when prefix doubling stopped
     bool lcp_from_keys = false;

@@ -91,6 +91,20 @@ __global__ void __launch_bounds__(kRNT) k_phi_emit(const unsigned *__restrict__ 
     bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
 }
 
+// isa[sa[r]] = r, emitted in SA order.
+__global__ void __launch_bounds__(kRNT) k_rank_emit(const unsigned *__restrict__ sa, long long n, BucketEmit be) {
+    __shared__ EmitSmem<kRNT, kRIPT> sm;
+    const long long r0 = (blockIdx.x * (long long)kRNT + threadIdx.x) * kRIPT;
+    unsigned dest[kRIPT], val[kRIPT];
+#pragma unroll
+    for (int q = 0; q < kRIPT; ++q) {
+        const long long r = r0 + q;
+        dest[q] = r < n ? sa[r] : kNoDest;
+        val[q] = (unsigned)r;
+    }
+    bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
+}
+
 // out[dest[i]] = val[i] for i < n (dest a permutation of its range).
 __global__ void __launch_bounds__(kRNT) k_pair_emit(const unsigned *__restrict__ dest_in,
                                                    const unsigned *__restrict__ val_in, long long n, BucketEmit be) {
@@ -153,6 +167,12 @@ void scatter_by(rs_ctx *c, const unsigned *dest, const unsigned *val, long long 
     BucketEmit be = bucket_setup(c, n_out, 0);
     RS_LAUNCH_B(c, 16.0 * n, k_pair_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0, dest, val, n, be);
     bucket_apply(c, be, out, n);
+}
+
+void scatter_rank(rs_ctx *c, const unsigned *sa, long long n, unsigned *isa) {
+    BucketEmit be = bucket_setup(c, n, 0);
+    RS_LAUNCH_B(c, 12.0 * n, k_rank_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0, sa, n, be);
+    bucket_apply(c, be, isa, n);
 }
 
 }  // namespace rsb

@@ -95,6 +95,8 @@ void bucket_apply(rs_ctx *c, const BucketEmit &be, unsigned *out, long long elem
 void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n);
 // phi[sa[j]] = sa[j-1] (0xffffffff at j = 0) through the bucketed scatter.
 void scatter_phi(rs_ctx *c, const unsigned *sa, long long n, unsigned *phi);
+// isa[sa[r]] = r through the bucketed scatter.
+void scatter_rank(rs_ctx *c, const unsigned *sa, long long n, unsigned *isa);
 // out[dest[i]] = val[i], i < n; dest a permutation into [0, n_out).
 void scatter_by(rs_ctx *c, const unsigned *dest, const unsigned *val, long long n, unsigned *out, long long n_out);
 

@@ -354,7 +354,10 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
         rr[j] = a > b ? a : b;
     }
     __syncthreads();
-    bucket_emit<kUNT, kUIPT>(be, vv, hh, s_emit, rr);
+    if (be.stage2)
+        bucket_emit<kUNT, kUIPT>(be, vv, hh, s_emit, rr);  // (ISA, raw) into text order
+    else
+        bucket_emit<kUNT, kUIPT>(be, vv, rr, s_emit);  // raw only: ISA is filled from SA if ever needed
 }
 
 // Pass 2 of reduce-then-scan over the k_update tiles: exclusive OpMaxSum
@@ -459,6 +462,13 @@ __global__ void k_lcp_patch(const u64 *__restrict__ stream, int b, const unsigne
         raw[sa[r - 1] + 1] = lp > h ? lp : h;
         raw[sa[r] + 1] = h > ln ? h : ln;
     }
+}
+
+// isa[V[t]] = H[t]: members of groups still tied keep their group head.
+__global__ void k_isa_heads(const unsigned *__restrict__ V, const unsigned *__restrict__ H, long long U,
+                            unsigned *__restrict__ isa) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t < U) isa[V[t]] = H[t];
 }
 
 // ---- small tied groups after round 0 ------------------------------------
@@ -656,6 +666,8 @@ __global__ void k_lcp_gather(const unsigned *__restrict__ sa, const unsigned *__
 
 }  // namespace
 
+void ensure_isa(rs_ctx *c);
+
 void build_suffix_array(rs_ctx *c, long long n) {
     const unsigned char *text = (const unsigned char *)c->bufs[B_TEXT].p;
     unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 4));
@@ -732,19 +744,31 @@ void build_suffix_array(rs_ctx *c, long long n) {
     long long U = n;
     const unsigned *P = nullptr;
     long long depth = K;
+    c->isa_lazy = false;
     while (true) {
         ++c->sa_rounds;
         long long tiles = (U + kUTile - 1) / kUTile;
         u64 *tagg = (u64 *)buf(c, B_BOUNDS, sizeof(u64) * 2 * (size_t)(tiles + 1));
         u64 *tpre = tagg + tiles + 1;
         BucketEmit be{nullptr, nullptr, 0, 0, nullptr};
-        if (!P) be = bucket_setup(c, n, 0, true);
-        else if (U >= n / 16) be = bucket_setup(c, n, 0, false);
+        bool skip_isa = false;
+        if (P && U >= n / 16) be = bucket_setup(c, n, 0, false);
+        // Round 0: the tied count is known after the reduce pass.  With few
+        // ties (i.i.d.-like text) the SA after round 0 + the small-group sort
+        // is final and the query pipeline never reads ISA -> scatter only raw
+        // and fill ISA from SA if it is ever needed.
+        auto setup_round0_emit = [&]() {
+            unsigned long long u0 = 0;
+            fetch_small(c, &u0, u_dev, sizeof(u0));
+            skip_isa = u0 <= (unsigned long long)(n / 8);
+            be = bucket_setup(c, n, 0, !skip_isa);
+        };
         // reduce-then-scan instead of a look-back: the heavy pass never waits
         if (ks32) {
             RS_LAUNCH_B(c, 4.0 * U, (k_update<true, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa, Pa,
                         Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
             RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
+            if (!P) setup_round0_emit();
             // round 0: 8 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
             RS_LAUNCH_B(c, 28.0 * U, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa,
                         Pa, Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
@@ -753,14 +777,17 @@ void build_suffix_array(rs_ctx *c, long long n) {
             RS_LAUNCH_B(c, 8.0 * U, (k_update<true, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha,
                         Va, tagg, tpre, lcp_d, bits, bits * K, be);
             RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
+            if (!P) setup_round0_emit();
             RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa,
                         isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
         }
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
         add_bytes_last(c, 4.0 * (double)un);
-        if (!P) bucket_apply(c, be, isa, n, raw, 1);
+        if (!P && skip_isa) bucket_apply(c, be, raw + 1, n);
+        else if (!P) bucket_apply(c, be, isa, n, raw, 1);
         else if (be.stage) bucket_apply(c, be, isa, U);
+        if (!P) c->isa_lazy = skip_isa;
         U = (long long)un;
         if (c->sa_rounds == 1 && U > 0 && U <= n / 8) {  // mostly small groups (i.i.d.-like text)
             // small tied groups: final order + LCP + raw by direct comparison;
@@ -789,6 +816,11 @@ void build_suffix_array(rs_ctx *c, long long n) {
             }
         }
         if (U == 0) break;
+        if (c->isa_lazy) {  // more rounds: they read ISA (group heads for the tied)
+            scatter_rank(c, sa, n, isa);
+            RS_LAUNCH(c, k_isa_heads, grid_for(U, 256), 256, 0, Va, Ha, U, isa);
+            c->isa_lazy = false;
+        }
         if (depth >= n) fail(RS_ECUDA, "suffix sort did not converge");
         std::swap(Pa, Pb);  // Pb/Hb/Vb now hold the unsorted slots, heads, suffixes
         std::swap(Ha, Hb);
@@ -839,6 +871,7 @@ void build_lcp(rs_ctx *c, long long n) {
     // PLCP -> SA order by ISA) go through the bucketed L2-local scatter
     // instead of one random 4-byte store/load per suffix.
     const bool bucketed = c->sa_device_built;
+    if (bucketed) ensure_isa(c);
     if (bucketed)
         scatter_phi(c, sa, n, phi);
     else
@@ -854,6 +887,14 @@ void build_lcp(rs_ctx *c, long long n) {
     } else {
         RS_LAUNCH_B(c, 12.0 * n, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
     }
+}
+
+// B_ISA from the final SA when round 0 skipped it (rank for the API, Kasai).
+void ensure_isa(rs_ctx *c) {
+    if (!c->isa_lazy) return;
+    const long long n = c->n;
+    scatter_rank(c, (const unsigned *)c->bufs[B_SA].p, n, (unsigned *)c->bufs[B_ISA].p);
+    c->isa_lazy = false;
 }
 
 }  // namespace rsb
