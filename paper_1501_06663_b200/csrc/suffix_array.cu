@@ -204,12 +204,9 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
     __shared__ u64 s_head_prefix;
     __shared__ u64 s_base;
     __shared__ EmitSmem<kUNT, kUIPT> s_emit;
-    unsigned *s_stage = s_emit.val;  // reused before the emit
     const long long tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
     const long long t0 = tile * kUTile + (long long)threadIdx.x * kUIPT;
-    const long long tile_t0 = tile * kUTile;
-    const int tile_n = (int)((U - tile_t0) < kUTile ? (U - tile_t0) : kUTile);
     u64 k[kUIPT];
     load_keys<KeyT>(keys, t0, U, k);
     u64 kprev = __shfl_up_sync(0xffffffffu, k[kUIPT - 1], 1);
@@ -315,12 +312,18 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
         }
         return;
     }
-    // ---- round 0: SA slots are t itself -> coalesced stores through shared memory ----
+    // ---- round 0: SA slots are t itself -> each thread stores its 8 slots as
+    //      two 16-byte vectors (a warp covers 1 KB contiguously) ----
+    const bool full = t0 + kUIPT <= U;
+    if (full) {
+        uint4 *d = reinterpret_cast<uint4 *>(sa + t0);
+        d[0] = make_uint4(vv[0], vv[1], vv[2], vv[3]);
+        d[1] = make_uint4(vv[4], vv[5], vv[6], vv[7]);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kUIPT; ++j) s_stage[threadIdx.x * kUIPT + j] = vv[j];
-    __syncthreads();
-    for (int i = threadIdx.x; i < tile_n; i += kUNT) sa[tile_t0 + i] = s_stage[i];
-    __syncthreads();
+        for (int j = 0; j < kUIPT; ++j)
+            if (t0 + j < U) sa[t0 + j] = vv[j];
+    }
     // LCP of adjacent suffixes from their packed K-symbol keys (capped by the
     // suffix lengths); kLcpUnknown (true LCP >= K) when undecided.
     const unsigned K = (unsigned)(key_bits / code_bits);
@@ -336,13 +339,19 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
         const unsigned vp = j ? vv[j - 1] : vprev;
         lk[j] = (t > 0 && t < U) ? key_lcp(k[j], j ? k[j - 1] : kprev, code_bits, key_bits, K, nn - vv[j], nn - vp)
                                  : 0;
-        s_stage[threadIdx.x * kUIPT + j] = lk[j];
     }
     lk[kUIPT] = (t0 + kUIPT < U)
                     ? key_lcp(knext, k[kUIPT - 1], code_bits, key_bits, K, nn - vnext, nn - vv[kUIPT - 1])
                     : 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < tile_n; i += kUNT) lcp_d[tile_t0 + i] = s_stage[i];
+    if (full) {
+        uint4 *d = reinterpret_cast<uint4 *>(lcp_d + t0);
+        d[0] = make_uint4(lk[0], lk[1], lk[2], lk[3]);
+        d[1] = make_uint4(lk[4], lk[5], lk[6], lk[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kUIPT; ++j)
+            if (t0 + j < U) lcp_d[t0 + j] = lk[j];
+    }
     // raw LLR candidate of each suffix: max(LCP with SA predecessor, with
     // successor); still-unknown pairs count as 0 and are fixed by k_lcp_patch
     // (every suffix of a tied group is next to one such pair).
