@@ -219,10 +219,18 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
     bool shortf[kUIPT + 2];  // shortness of items j-1 .. j+... (index j+1)
     if (!P) {
         const unsigned Ks = (unsigned)(key_bits / code_bits);
+        if (t0 + kUIPT <= U) {  // two 16-byte loads
+            const uint4 *q = reinterpret_cast<const uint4 *>(vals + t0);
+            const uint4 a = q[0], b = q[1];
+            const unsigned w[kUIPT] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int j = 0; j < kUIPT; ++j) {
-            const long long t = t0 + j;
-            shortf[j + 1] = t < U && (unsigned)(U - vals[t]) < Ks;
+            for (int j = 0; j < kUIPT; ++j) shortf[j + 1] = (unsigned)(U - w[j]) < Ks;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kUIPT; ++j) {
+                const long long t = t0 + j;
+                shortf[j + 1] = t < U && (unsigned)(U - vals[t]) < Ks;
+            }
         }
         const long long tp = t0 - 1, tn = t0 + kUIPT;
         shortf[0] = tp >= 0 && (unsigned)(U - vals[tp]) < Ks;
