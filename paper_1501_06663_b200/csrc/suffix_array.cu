@@ -213,39 +213,19 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
     u64 knext = __shfl_down_sync(0xffffffffu, k[0], 1);
     if (lane == 0) kprev = (t0 > 0 && t0 - 1 < U) ? (u64)keys[t0 - 1] : 0;
     if (lane == 31) knext = (t0 + kUIPT < U) ? (u64)keys[t0 + kUIPT] : 0;
-    // round 0: a short suffix (fewer than K symbols) is never tied -- its
-    // padded key may equal longer suffixes' keys, but the input order already
-    // placed it correctly (k_init_keys), so it forms its own group.
-    bool shortf[kUIPT + 2];  // shortness of items j-1 .. j+... (index j+1)
-    if (!P) {
-        const unsigned Ks = (unsigned)(key_bits / code_bits);
-        if (t0 + kUIPT <= U) {  // two 16-byte loads
-            const uint4 *q = reinterpret_cast<const uint4 *>(vals + t0);
-            const uint4 a = q[0], b = q[1];
-            const unsigned w[kUIPT] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-            for (int j = 0; j < kUIPT; ++j) shortf[j + 1] = (unsigned)(U - w[j]) < Ks;
-        } else {
-#pragma unroll
-            for (int j = 0; j < kUIPT; ++j) {
-                const long long t = t0 + j;
-                shortf[j + 1] = t < U && (unsigned)(U - vals[t]) < Ks;
-            }
-        }
-        const long long tp = t0 - 1, tn = t0 + kUIPT;
-        shortf[0] = tp >= 0 && (unsigned)(U - vals[tp]) < Ks;
-        shortf[kUIPT + 1] = tn < U && (unsigned)(U - vals[tn]) < Ks;
-    } else {
-#pragma unroll
-        for (int j = 0; j < kUIPT + 2; ++j) shortf[j] = false;
-    }
+    // Round 0: a suffix shorter than K symbols (padded key) may tie with the
+    // longer suffixes it is a prefix of.  It sorts first among them (the input
+    // order puts short suffixes first, shortest first) and stays there, so the
+    // key LCPs next to it (capped by its length) are final; the group is then
+    // resolved like any other (the direct comparison stops at its end, later
+    // rounds key it by its length).
     bool newf[kUIPT + 1];
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) {
         long long t = t0 + j;
-        newf[j] = (t == 0) || (k[j] != (j ? k[j - 1] : kprev)) || shortf[j] || shortf[j + 1];
+        newf[j] = (t == 0) || (k[j] != (j ? k[j - 1] : kprev));
     }
-    newf[kUIPT] = (t0 + kUIPT >= U) || (knext != k[kUIPT - 1]) || shortf[kUIPT] || shortf[kUIPT + 1];
+    newf[kUIPT] = (t0 + kUIPT >= U) || (knext != k[kUIPT - 1]);
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j)
         if (t0 + j + 1 == U) newf[j + 1] = true;
@@ -838,7 +818,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
             RS_LAUNCH(c, k_isa_heads, grid_for(U, 256), 256, 0, Va, Ha, U, isa);
             c->isa_lazy = false;
         }
-        if (depth >= n) fail(RS_ECUDA, "suffix sort did not converge");
+        if (depth > 2 * n + 64) fail(RS_ECUDA, "suffix sort did not converge");  // depth >= n resolves every group
         std::swap(Pa, Pb);  // Pb/Hb/Vb now hold the unsorted slots, heads, suffixes
         std::swap(Ha, Hb);
         std::swap(Va, Vb);
