@@ -358,43 +358,61 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
 }
 
 // Pass 2 of reduce-then-scan over the k_update tiles: exclusive OpMaxSum
-// prefix per tile (one block; a few hundred thousand tiles at most) and the
-// total unsorted count.
-__global__ void __launch_bounds__(1024) k_tile_scan(const u64 *__restrict__ agg, long long tiles,
-                                                    u64 *__restrict__ prefix, unsigned long long *U_next) {
-    __shared__ u64 s_w[32];
+// prefix per tile and the total unsorted count.  256 threads x 4 aggregates
+// per block, block scan, decoupled look-back across blocks (a single-block
+// scan was latency-bound at ~0.25 ms for 131k tiles).
+constexpr int kTSNT = 256, kTSIPT = 4, kTSTile = kTSNT * kTSIPT;
+__global__ void __launch_bounds__(kTSNT) k_tile_scan_lb(const u64 *__restrict__ agg, long long tiles,
+                                                        u64 *__restrict__ prefix, unsigned long long *U_next,
+                                                        unsigned *counter, u64 *status, long long blocks) {
+    __shared__ unsigned s_blk;
+    __shared__ u64 s_warp[kTSNT / 32];
+    __shared__ u64 s_base;
     const OpMaxSum op;
-    const long long per = (tiles + 1023) / 1024;
-    const long long a = threadIdx.x * per, b = a + per < tiles ? a + per : tiles;
-    u64 acc = 0;
-    for (long long t = a; t < b; ++t) acc = op(acc, agg[t]);
-    // block exclusive scan of acc with op
+    if (threadIdx.x == 0) s_blk = atomicAdd(counter, 1u);
+    __syncthreads();
+    const long long blk = s_blk;
+    const long long i0 = blk * kTSTile + (long long)threadIdx.x * kTSIPT;
+    u64 v[kTSIPT], acc = 0;
+#pragma unroll
+    for (int j = 0; j < kTSIPT; ++j) {
+        v[j] = i0 + j < tiles ? agg[i0 + j] : 0ull;
+        acc = op(acc, v[j]);
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u64 x = acc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        const u64 y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x = op(x, y);
     }
-    if (lane == 31) s_w[warp] = x;
+    if (lane == 31) s_warp[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        u64 w = s_w[lane];
+        u64 w = lane < kTSNT / 32 ? s_warp[lane] : 0ull;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            u64 y = __shfl_up_sync(0xffffffffu, w, o);
+            const u64 y = __shfl_up_sync(0xffffffffu, w, o);
             if (lane >= o) w = op(w, y);
         }
-        s_w[lane] = w;
+        if (lane < kTSNT / 32) s_warp[lane] = w;
+        const u64 total = __shfl_sync(0xffffffffu, w, kTSNT / 32 - 1);
+        const u64 base = lookback_warp(status, blk, total, op);
+        if (lane == 0) {
+            s_base = base;
+            if (blk == blocks - 1) *U_next = op(base, total) & ((1ull << 31) - 1);
+        }
     }
     __syncthreads();
-    u64 run = op(warp ? s_w[warp - 1] : 0ull, __shfl_up_sync(0xffffffffu, x, 1));
-    if (lane == 0) run = warp ? s_w[warp - 1] : 0ull;
-    for (long long t = a; t < b; ++t) {
-        prefix[t] = run;
-        run = op(run, agg[t]);
+    // exclusive prefix of this thread's first aggregate
+    u64 run = op(s_base, warp ? s_warp[warp - 1] : 0ull);
+    const u64 xprev = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane) run = op(run, xprev);
+#pragma unroll
+    for (int j = 0; j < kTSIPT; ++j) {
+        if (i0 + j < tiles) prefix[i0 + j] = run;
+        run = op(run, v[j]);
     }
-    if (threadIdx.x == 1023) *U_next = s_w[31] & ((1ull << 31) - 1);
 }
 
 // 64 bits of the packed symbol stream starting at symbol p.
@@ -754,6 +772,12 @@ void build_suffix_array(rs_ctx *c, long long n) {
         // ties (i.i.d.-like text) the SA after round 0 + the small-group sort
         // is final and the query pipeline never reads ISA -> scatter only raw
         // and fill ISA from SA if it is ever needed.
+        auto tile_scan = [&](const u64 *agg, long long nt, u64 *pre) {
+            const long long blocks = (nt + kTSTile - 1) / kTSTile;
+            Scratch sc = scratch(c, blocks);
+            RS_LAUNCH(c, k_tile_scan_lb, (unsigned)blocks, kTSNT, 0, agg, nt, pre, u_dev, sc.counter, sc.status,
+                      blocks);
+        };
         auto setup_round0_emit = [&]() {
             unsigned long long u0 = 0;
             fetch_small(c, &u0, u_dev, sizeof(u0));
@@ -764,7 +788,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
         if (ks32) {
             RS_LAUNCH_B(c, 4.0 * U, (k_update<true, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa, Pa,
                         Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
-            RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
+            tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
             // round 0: 8 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
             RS_LAUNCH_B(c, 28.0 * U, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa,
@@ -773,7 +797,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
         } else {
             RS_LAUNCH_B(c, 8.0 * U, (k_update<true, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha,
                         Va, tagg, tpre, lcp_d, bits, bits * K, be);
-            RS_LAUNCH(c, k_tile_scan, 1, 1024, 0, tagg, tiles, tpre, u_dev);
+            tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
             RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa,
                         isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
