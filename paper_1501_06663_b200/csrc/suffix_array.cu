@@ -549,9 +549,9 @@ __global__ void k_small_groups(const unsigned *__restrict__ H, const unsigned *_
         if (swap) {
             sa[head] = y;
             sa[head + 1] = x;
-            isa[y] = head;
+            if (isa) isa[y] = head;
         }
-        isa[second] = head + 1;
+        if (isa) isa[second] = head + 1;
         lcp_d[head + 1] = l;
         raw[first + 1] = lb > l ? lb : l;
         raw[second + 1] = l > le ? l : le;
@@ -579,7 +579,7 @@ __global__ void k_small_groups(const unsigned *__restrict__ H, const unsigned *_
     for (int j = 0; j < s; ++j) {
         const unsigned slot = head + j;
         sa[slot] = v[j];
-        isa[v[j]] = slot;
+        if (isa) isa[v[j]] = slot;
         if (j) lcp_d[slot] = lc[j];
         raw[v[j] + 1] = lc[j] > lc[j + 1] ? lc[j] : lc[j + 1];
     }
@@ -814,8 +814,9 @@ void build_suffix_array(rs_ctx *c, long long n) {
             // small tied groups: final order + LCP + raw by direct comparison;
             // the lists keep only the larger groups (order preserved)
             unsigned *keep = (unsigned *)buf(c, B_T4, sizeof(unsigned) * (size_t)U);
+            // lazy ISA (rebuilt from the final SA if ever needed): no ISA stores here
             RS_LAUNCH_B(c, 16.0 * U, k_small_groups, grid_for(U, 256), 256, 0, Ha, Va, U, stream, bits, n,
-                        (long long)K, sa, isa, lcp_d, raw, keep);
+                        (long long)K, sa, c->isa_lazy ? nullptr : isa, lcp_d, raw, keep);
             const long long ktiles = (U + kKTile - 1) / kKTile;
             Scratch ks_ = scratch(c, ktiles);
             RS_LAUNCH_B(c, 16.0 * U, k_keep_compact, (unsigned)ktiles, kKNT, 0, keep, Pa, Ha, Va, U, Pb, Hb, Vb, u_dev,
