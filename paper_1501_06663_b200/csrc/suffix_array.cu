@@ -351,10 +351,17 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
         rr[j] = a > b ? a : b;
     }
     __syncthreads();
-    if (be.stage2)
+    if (be.stage2) {
         bucket_emit<kUNT, kUIPT>(be, vv, hh, s_emit, rr);  // (ISA, raw) into text order
-    else
-        bucket_emit<kUNT, kUIPT>(be, vv, rr, s_emit);  // raw only: ISA is filled from SA if ever needed
+    } else {
+        // raw only (ISA is filled from SA if ever needed); the tied suffixes'
+        // raw is emitted by k_small_groups into the same buckets
+#pragma unroll
+        for (int j = 0; j < kUIPT; ++j)
+            if (unsorted >> j & 1) hh[j] = kNoDest;
+            else hh[j] = vv[j];
+        bucket_emit<kUNT, kUIPT>(be, hh, rr, s_emit);
+    }
 }
 
 // Pass 2 of reduce-then-scan over the k_update tiles: exclusive OpMaxSum
@@ -522,67 +529,103 @@ __device__ __forceinline__ bool suffix_less(const u64 *__restrict__ stream, int 
 // One thread per list entry (groups are runs of equal heads; a group's slots
 // are head .. head+s-1).  Each entry classifies its group by looking at most
 // kSmallGroup entries each way; the first entry of a small group sorts it.
-// keep[t] = 1 marks entries of groups left to the doubling rounds.
-__global__ void k_small_groups(const unsigned *__restrict__ H, const unsigned *__restrict__ V, long long U,
-                               const u64 *__restrict__ stream, int b, long long n, long long K,
-                               unsigned *__restrict__ sa, unsigned *__restrict__ isa, unsigned *__restrict__ lcp_d,
-                               unsigned *__restrict__ raw, unsigned *__restrict__ keep) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= U) return;
-    const unsigned head = H[t];
-    int back = 0, fwd = 0;
-    while (back < kSmallGroup && t - back - 1 >= 0 && H[t - back - 1] == head) ++back;
-    while (fwd < kSmallGroup && t + fwd + 1 < U && H[t + fwd + 1] == head) ++fwd;
-    const bool small = back + fwd + 1 <= kSmallGroup;
-    keep[t] = small ? 0u : 1u;
-    if (!small || back) return;
-    const int s = fwd + 1;
-    const unsigned lb = lcp_d[head];  // group boundaries: keys differ there, LCP known from round 0
-    if (s == 2) {
-        // round 0 left sa[head..head+1] = (x, y), isa = head for both, and
-        // raw without the (unknown) inner LCP; write only what changes
-        const unsigned x = V[t], y = V[t + 1];
-        const unsigned le = lcp_d[head + 2];
-        unsigned l;
-        const bool swap = suffix_less(stream, b, n, K, y, x, l);
-        const unsigned first = swap ? y : x, second = swap ? x : y;
-        if (swap) {
-            sa[head] = y;
-            sa[head + 1] = x;
-            if (isa) isa[y] = head;
+// keep[t] = 1 marks entries of groups left to the doubling rounds.  The raw
+// LLR corrections (text order, random) leave through the bucketed scatter:
+// each member's (suffix, raw) is handed to its own entry's thread in shared
+// memory and the block emits them together (be; applied after round 0's raw).
+constexpr int kSGNT = 256;
+__device__ __forceinline__ void sg_put(long long e, long long tb, unsigned v, unsigned r, unsigned *s_dest,
+                                       unsigned *s_val, unsigned *__restrict__ raw) {
+    if (e - tb < kSGNT) {
+        s_dest[e - tb] = v;
+        s_val[e - tb] = r;
+    } else {
+        raw[v + 1] = r;  // member beyond this block (rare): direct store
+    }
+}
+
+__global__ void __launch_bounds__(kSGNT) k_small_groups(const unsigned *__restrict__ P,
+                                                        const unsigned *__restrict__ H,
+                                                        const unsigned *__restrict__ V, long long U,
+                                                        const u64 *__restrict__ stream, int b, long long n,
+                                                        long long K, unsigned *__restrict__ sa,
+                                                        unsigned *__restrict__ isa, unsigned *__restrict__ lcp_d,
+                                                        unsigned *__restrict__ raw, unsigned *__restrict__ keep,
+                                                        BucketEmit be) {
+    __shared__ EmitSmem<kSGNT, 1> s_emit;
+    __shared__ unsigned s_dest[kSGNT], s_val[kSGNT];
+    const long long tb = blockIdx.x * (long long)kSGNT;
+    const long long t = tb + threadIdx.x;
+    s_dest[threadIdx.x] = kNoDest;
+    __syncthreads();
+    if (t < U) {
+        const unsigned head = H[t];
+        int back = 0, fwd = 0;
+        while (back < kSmallGroup && t - back - 1 >= 0 && H[t - back - 1] == head) ++back;
+        while (fwd < kSmallGroup && t + fwd + 1 < U && H[t + fwd + 1] == head) ++fwd;
+        const bool small = back + fwd + 1 <= kSmallGroup;
+        keep[t] = small ? 0u : 1u;
+        if (!small) {  // left to the doubling rounds: round-0 raw candidate (unknown LCPs as 0)
+            const unsigned slot = P[t];
+            unsigned a = lcp_d[slot], c2 = lcp_d[slot + 1];
+            a = a == kLcpUnknown ? 0u : a;
+            c2 = c2 == kLcpUnknown ? 0u : c2;
+            s_dest[threadIdx.x] = V[t];
+            s_val[threadIdx.x] = a > c2 ? a : c2;
         }
-        if (isa) isa[second] = head + 1;
-        lcp_d[head + 1] = l;
-        raw[first + 1] = lb > l ? lb : l;
-        raw[second + 1] = l > le ? l : le;
-        return;
-    }
-    unsigned v[kSmallGroup];
-    unsigned lc[kSmallGroup + 1];
-    lc[0] = lb;
-    lc[s] = lcp_d[head + s];
-    for (int j = 0; j < s; ++j) v[j] = V[t + j];
-    unsigned l;
-    for (int i = 1; i < s; ++i) {  // insertion sort by suffix comparison
-        const unsigned x = v[i];
-        int j = i;
-        while (j > 0 && suffix_less(stream, b, n, K, x, v[j - 1], l)) {
-            v[j] = v[j - 1];
-            --j;
+        if (small && !back) {
+            const int s = fwd + 1;
+            const unsigned lb = lcp_d[head];  // group boundaries: keys differ there, LCP known from round 0
+            if (s == 2) {
+                // round 0 left sa[head..head+1] = (x, y), isa = head for both, and
+                // raw without the (unknown) inner LCP; write only what changes
+                const unsigned x = V[t], y = V[t + 1];
+                const unsigned le = lcp_d[head + 2];
+                unsigned l;
+                const bool swap = suffix_less(stream, b, n, K, y, x, l);
+                const unsigned first = swap ? y : x, second = swap ? x : y;
+                if (swap) {
+                    sa[head] = y;
+                    sa[head + 1] = x;
+                    if (isa) isa[y] = head;
+                }
+                if (isa) isa[second] = head + 1;
+                lcp_d[head + 1] = l;
+                sg_put(t, tb, first, lb > l ? lb : l, s_dest, s_val, raw);
+                sg_put(t + 1, tb, second, l > le ? l : le, s_dest, s_val, raw);
+            } else {
+                unsigned v[kSmallGroup];
+                unsigned lc[kSmallGroup + 1];
+                lc[0] = lb;
+                lc[s] = lcp_d[head + s];
+                for (int j = 0; j < s; ++j) v[j] = V[t + j];
+                unsigned l;
+                for (int i = 1; i < s; ++i) {  // insertion sort by suffix comparison
+                    const unsigned x = v[i];
+                    int j = i;
+                    while (j > 0 && suffix_less(stream, b, n, K, x, v[j - 1], l)) {
+                        v[j] = v[j - 1];
+                        --j;
+                    }
+                    v[j] = x;
+                }
+                for (int j = 1; j < s; ++j) {
+                    suffix_less(stream, b, n, K, v[j - 1], v[j], l);
+                    lc[j] = l;
+                }
+                for (int j = 0; j < s; ++j) {
+                    const unsigned slot = head + j;
+                    sa[slot] = v[j];
+                    if (isa) isa[v[j]] = slot;
+                    if (j) lcp_d[slot] = lc[j];
+                    sg_put(t + j, tb, v[j], lc[j] > lc[j + 1] ? lc[j] : lc[j + 1], s_dest, s_val, raw);
+                }
+            }
         }
-        v[j] = x;
     }
-    for (int j = 1; j < s; ++j) {
-        suffix_less(stream, b, n, K, v[j - 1], v[j], l);
-        lc[j] = l;
-    }
-    for (int j = 0; j < s; ++j) {
-        const unsigned slot = head + j;
-        sa[slot] = v[j];
-        if (isa) isa[v[j]] = slot;
-        if (j) lcp_d[slot] = lc[j];
-        raw[v[j] + 1] = lc[j] > lc[j + 1] ? lc[j] : lc[j + 1];
-    }
+    __syncthreads();
+    const unsigned d = s_dest[threadIdx.x], vl = s_val[threadIdx.x];
+    bucket_emit<kSGNT, 1>(be, &d, &vl, s_emit);
 }
 
 // Order-preserving compaction of the (slot, head, suffix) lists to the kept
@@ -805,9 +848,13 @@ void build_suffix_array(rs_ctx *c, long long n) {
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
         add_bytes_last(c, 4.0 * (double)un);
-        if (!P && skip_isa) bucket_apply(c, be, raw + 1, n);
-        else if (!P) bucket_apply(c, be, isa, n, raw, 1);
-        else if (be.stage) bucket_apply(c, be, isa, U);
+        // skip_isa (few ties): raw is applied after k_small_groups added the tied suffixes
+        if (!P) {
+            if (!skip_isa) bucket_apply(c, be, isa, n, raw, 1);
+            else if (un == 0) bucket_apply(c, be, raw + 1, n);
+        } else if (be.stage) {
+            bucket_apply(c, be, isa, U);
+        }
         if (!P) c->isa_lazy = skip_isa;
         U = (long long)un;
         if (c->sa_rounds == 1 && U > 0 && U <= n / 8) {  // mostly small groups (i.i.d.-like text)
@@ -815,8 +862,10 @@ void build_suffix_array(rs_ctx *c, long long n) {
             // the lists keep only the larger groups (order preserved)
             unsigned *keep = (unsigned *)buf(c, B_T4, sizeof(unsigned) * (size_t)U);
             // lazy ISA (rebuilt from the final SA if ever needed): no ISA stores here
-            RS_LAUNCH_B(c, 16.0 * U, k_small_groups, grid_for(U, 256), 256, 0, Ha, Va, U, stream, bits, n,
-                        (long long)K, sa, c->isa_lazy ? nullptr : isa, lcp_d, raw, keep);
+            // (the tied suffixes' raw goes into round 0's buckets, applied once below)
+            RS_LAUNCH_B(c, 16.0 * U, k_small_groups, grid_for(U, kSGNT), kSGNT, 0, Pa, Ha, Va, U, stream, bits, n,
+                        (long long)K, sa, c->isa_lazy ? nullptr : isa, lcp_d, raw, keep, be);
+            bucket_apply(c, be, raw + 1, n);
             const long long ktiles = (U + kKTile - 1) / kKTile;
             Scratch ks_ = scratch(c, ktiles);
             RS_LAUNCH_B(c, 16.0 * U, k_keep_compact, (unsigned)ktiles, kKNT, 0, keep, Pa, Ha, Va, U, Pb, Hb, Vb, u_dev,
