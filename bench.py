@@ -297,8 +297,10 @@ def run_single(args) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
         "data": "synthetic",
         "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
-                   "pipeline": "SA(prefix doubling, onesweep LSD radix) + rank + LCP(PLCP) + "
-                               "raw LLR + fused compaction + all-ties scan (TMA-staged)",
+                   "pipeline": "SA (prefix doubling: onesweep LSD radix, small tied groups sorted "
+                               "directly) + LCP (round-0 keys + direct comparison; Kasai for "
+                               "repetitive text) + raw LLR + compaction fused into the all-ties "
+                               "scan (TMA-staged)",
                    "parallelism": "single GPU", "l2": "input 256 MiB > 126 MB L2; all arrays "
                                                      "rebuilt each step",
                    "T": T, "sa_rounds": rounds},

@@ -16,8 +16,8 @@ python bench.py --impl reference > "$out/bench_ref.json" 2> "$out/bench_ref.err"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file "$out/launches.csv" \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > "$out/ncu_launches.log" 2>&1
 python tools/ncu_step.py > "$out/step_plain.log" 2>&1 || exit 1
-for spec in "k_onesweep 2 onesweep" "k_query 0 query" "k_update 1 update" "k_bucket_apply 0 bucket_apply" \
-            "k_lcp_patch 0 lcp_patch" "k_compact_raw 0 compact_raw"; do
+for spec in "k_onesweep 2 onesweep" "k_query_fused 0 query" "k_update 1 update" "k_bucket_apply 0 bucket_apply" \
+            "k_small_groups 0 small_groups" "k_onesweep 0 onesweep_text"; do
   set -- $spec
   ncu --set full --clock-control none --import-source on -k regex:$1 --launch-skip $2 -c 1 \
       -o "$out/$3" python tools/ncu_step.py > "$out/$3.log" 2>&1
