@@ -150,11 +150,14 @@ def _view(ctx: _native.Context, which: int, count: int, typestr: str, device):
 
 
 def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None,
-                          timings: dict | None = None):
+                          timings: dict | None = None, resident: bool = False, gather: bool = True):
     """Distributed query.  `data` (uint8 text) is needed on rank 0 only.
 
     Returns torch device tensors of the reference layout on rank 0
     ((starts, lengths) or (lengths, offsets, flat)), None elsewhere.
+    resident=True: rank 0 reuses the text already on its device (derived
+    arrays are rebuilt); gather=False: every rank keeps its shard of the
+    answer (rebased CSR) in its own HBM and the call returns None.
     """
     import torch
     import torch.distributed as dist
@@ -168,9 +171,13 @@ def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None
         # 1. rank 0: text -> SA -> LCP -> raw LLR -> LLRc on its GPU
         meta = torch.zeros(2, dtype=torch.int64, device=device)
         if rank == 0:
-            host = np.ascontiguousarray(data, dtype=np.uint8)
-            n = int(host.size)
-            ctx.call("rs_set_text", _native.u8(host), n)
+            if resident:
+                n = int(data.size)
+                ctx.call("rs_clear_derived")
+            else:
+                host = np.ascontiguousarray(data, dtype=np.uint8)
+                n = int(host.size)
+                ctx.call("rs_set_text", _native.u8(host), n)
             m_arr = np.zeros(1, np.int64)
             ctx.call("rs_get_compact_size", _native.i64(m_arr))
             ctx.synchronize()
@@ -194,12 +201,18 @@ def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None
             bases = tie_bases(totals)
             ctx.call("rs_shard_rebase", bases[rank])
             T_all = sum(totals)
+            if not gather:
+                ctx.synchronize()
+                return None
             a = _view(ctx, _native.BUF_OUT0, cnt, "<i8", device)
             b = _view(ctx, _native.BUF_OUT1, cnt + 1, "<i8", device)
             f = _view(ctx, _native.BUF_FLAT, int(total[0]), "<i8", device)
             ctx.synchronize()
             out = gather_shards(n, mode, lo, hi, a, b, f, T_all, bases[rank], group, device)
         else:
+            if not gather:
+                ctx.synchronize()
+                return None
             a = _view(ctx, _native.BUF_OUT0, cnt, "<i8", device)
             b = _view(ctx, _native.BUF_OUT1, cnt, "<i8", device)
             ctx.synchronize()
@@ -208,20 +221,42 @@ def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None
     return out
 
 
+def _to_host(t):
+    """One D2H of a device tensor into a pooled pinned numpy array (full PCIe rate)."""
+    import torch
+    arr = _native.pinned_pool.empty(int(t.numel()), np.int64)
+    if arr.size:
+        torch.from_numpy(arr).copy_(t, non_blocking=True)
+    return arr
+
+
 def to_answers(out, mode: str):
-    """Rank-0 tensors -> reference dataclasses (one D2H each)."""
+    """Rank-0 tensors -> reference dataclasses (one D2H each, pinned)."""
+    import torch
     from paper_1501_06663_b200.query import AllAnswers, LeftmostAnswers
     if mode == "leftmost":
         s, l = out
-        return LeftmostAnswers(starts=s.cpu().numpy(), lengths=l.cpu().numpy())
-    l, o, f = out
-    return AllAnswers(lengths=l.cpu().numpy(), offsets=o.cpu().numpy(), flat_starts=f.cpu().numpy())
+        res = LeftmostAnswers(starts=_to_host(s), lengths=_to_host(l))
+    else:
+        l, o, f = out
+        res = AllAnswers(lengths=_to_host(l), offsets=_to_host(o), flat_starts=_to_host(f))
+    torch.cuda.synchronize()
+    return res
 
 
 # ---------------------------------------------------------------------------------------
 # bench (torchrun, N > 1)
 # ---------------------------------------------------------------------------------------
 def bench_main(args) -> None:
+    """torchrun bench (N > 1), strong scaling over one text.
+
+    value: device-resident step -- rank 0 holds the text in HBM and rebuilds
+    SA -> LLRc, LLRc is broadcast over NVLink, every rank scans its position
+    shard and keeps its rebased CSR shard in its own HBM (as the N = 1 step
+    keeps the whole answer); CUDA events on the library stream, max over ranks.
+    e2e: the full API-level call -- text H2D, the same path, shards gathered
+    to rank 0 over NVLink and one D2H into the reference int64 arrays.
+    """
     import json
 
     import torch
@@ -229,44 +264,57 @@ def bench_main(args) -> None:
 
     from paper_1501_06663_b200 import workloads
 
+    # NCCL's own messages (e.g. its version banner) go to stderr: stdout
+    # carries exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
     data = workloads.make(args.config, args.n) if rank == 0 else None
-    n = int(data.size) if rank == 0 else 0
+    ctx = _native.context(local)
+    if rank == 0:
+        host = np.ascontiguousarray(data, dtype=np.uint8)
+        with ctx.lock:
+            ctx.call("rs_set_text", _native.u8(host), int(host.size))
 
     def step():
-        return sharded_all_positions(data, "all")
+        sharded_all_positions(data, "all", resident=True, gather=False)
 
     for _ in range(args.warmup):
         step()
     dist.barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    l0 = ctx.launches()
+    ctx.record(0)
     for _ in range(args.steps):
-        out = step()
-    ev1.record()
+        step()
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ctx.record(1)
+    ms = ctx.elapsed_ms(0, 1) / args.steps
+    launches = (ctx.launches() - l0) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    nn = torch.tensor([n], dtype=torch.int64, device="cuda")
+    nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device="cuda")
     dist.broadcast(nn, src=0)
     n = int(nn.item())
-    # e2e: H2D of the text on rank 0 (inside rs_set_text) + final D2H of the CSR
+    lt = torch.tensor([launches], dtype=torch.float64, device="cuda")
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    # e2e: H2D of the text on rank 0 (inside rs_set_text) + gather + final D2H of the CSR
     e2e = []
-    for _ in range(max(1, args.steps)):
+    res = None
+    for i in range(args.warmup + max(1, args.steps)):  # warm-up fills the pinned result pool
+        res = out = None
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = step()
+        out = sharded_all_positions(data, "all")
         res = to_answers(out, "all") if rank == 0 else None
         torch.cuda.synchronize()
         dist.barrier()
-        e2e.append(time.perf_counter() - t0)
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t0)
     if rank == 0:
         T = int(res.flat_starts.size)
         line = {
@@ -276,11 +324,14 @@ def bench_main(args) -> None:
             "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
             "data": "synthetic",
             "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
-                       "parallelism": f"position shards x{world} (SA/LLRc on rank 0, NCCL broadcast)",
+                       "parallelism": f"position shards x{world} (SA/LLRc on rank 0, NCCL broadcast; "
+                                      "CSR shards stay on their GPUs)",
+                       "l2": "input 256 MiB > 126 MB L2; all arrays rebuilt each step",
                        "T": T},
-            "gpu_launches": None,
+            "gpu_launches": int(round(float(lt.item()) * args.steps)),
             "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": n,
-                    "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T},
+                    "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
+                    "path": "sharded_all_positions + NCCL gather to rank 0 + D2H"},
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
