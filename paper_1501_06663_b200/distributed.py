@@ -264,9 +264,12 @@ def bench_main(args) -> None:
 
     from paper_1501_06663_b200 import workloads
 
-    # NCCL's own messages (e.g. its version banner) go to stderr: stdout
-    # carries exactly one JSON line
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    # stdout carries exactly one JSON line: everything else written to fd 1
+    # (e.g. the NCCL version banner at communicator creation) goes to stderr
+    import sys
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -333,6 +336,9 @@ def bench_main(args) -> None:
                     "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
                     "path": "sharded_all_positions + NCCL gather to rank 0 + D2H"},
         }
-        print(json.dumps(line), flush=True)
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
     dist.destroy_process_group()
+    sys.stdout.flush()
+    os.dup2(json_fd, 1)
+    os.close(json_fd)
