@@ -379,6 +379,22 @@ __device__ __forceinline__ u64 text_key(const TextKeys &tk, long long p) {
 __device__ __forceinline__ long long text_pos(const TextKeys &tk, long long e) {
     return e < tk.S ? tk.n - 1 - e : e - tk.S;
 }
+// Text prepared for the suffix sort (suffix_array.cu prepare_text).
+struct TextPrep {
+    u64 *stream;      // B_PACKED: b-bit codes, zero padded
+    long long words;  // stream words incl. padding
+    int bits, K, sigma;
+};
+TextPrep prepare_text(rs_ctx *c, long long n);
+
+// Round-0 update over one rank's contiguous segment of the suffix array: the
+// text length and the LCPs with the neighbouring segments' boundary suffixes
+// (0 at the ends of the whole array).
+struct SegBoundary {
+    long long n_text;
+    unsigned lcp_first, lcp_last;
+};
+
 // Sorts (keys, vals) pairs by the low `bits` bits of keys, stable.  With tk,
 // the input pairs are generated from the packed text (keys/vals unread).
 template <typename KeyT>

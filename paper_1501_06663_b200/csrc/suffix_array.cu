@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
                                                  unsigned *__restrict__ V_next, u64 *__restrict__ tile_agg,
                                                  const u64 *__restrict__ tile_prefix,
                                                  unsigned *__restrict__ lcp_d, int code_bits, int key_bits,
-                                                 BucketEmit be) {
+                                                 BucketEmit be, SegBoundary sb) {
     __shared__ u64 s_warp[kUNT / 32];
     __shared__ unsigned s_warp32[kUNT / 32];
     __shared__ u64 s_head_prefix;
@@ -319,18 +319,21 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
     unsigned vnext = __shfl_down_sync(0xffffffffu, vv[0], 1);
     if (lane == 0) vprev = t0 > 0 ? vals[t0 - 1] : 0;
     if (lane == 31) vnext = (t0 + kUIPT < U) ? vals[t0 + kUIPT] : 0;
-    const unsigned nn = (unsigned)U;  // round 0: U == n
+    // text length (remaining lengths cap the key LCPs); U == n unless this is
+    // one rank's segment of a distributed sort, whose first slot and the slot
+    // after its last hold the LCPs with the neighbouring segments (sb)
+    const unsigned nn = (unsigned)sb.n_text;
     unsigned lk[kUIPT + 1];
 #pragma unroll
     for (int j = 0; j < kUIPT; ++j) {
         long long t = t0 + j;
         const unsigned vp = j ? vv[j - 1] : vprev;
         lk[j] = (t > 0 && t < U) ? key_lcp(k[j], j ? k[j - 1] : kprev, code_bits, key_bits, K, nn - vv[j], nn - vp)
-                                 : 0;
+                : t == 0 ? sb.lcp_first : sb.lcp_last;
     }
     lk[kUIPT] = (t0 + kUIPT < U)
                     ? key_lcp(knext, k[kUIPT - 1], code_bits, key_bits, K, nn - vnext, nn - vv[kUIPT - 1])
-                    : 0;
+                    : sb.lcp_last;
     if (full) {
         uint4 *d = reinterpret_cast<uint4 *>(lcp_d + t0);
         d[0] = make_uint4(lk[0], lk[1], lk[2], lk[3]);
@@ -724,18 +727,12 @@ __global__ void k_lcp_gather(const unsigned *__restrict__ sa, const unsigned *__
 
 }  // namespace
 
-void ensure_isa(rs_ctx *c);
-
-void build_suffix_array(rs_ctx *c, long long n) {
+// Alphabet -> order-preserving codes, round-0 key length K, and the text
+// packed once as a big-endian stream of b-bit codes (n b/8 bytes, L2-resident
+// at 256 Mi DNA); the sort's histogram and first pass generate (key, suffix)
+// pairs from it directly.
+TextPrep prepare_text(rs_ctx *c, long long n) {
     const unsigned char *text = (const unsigned char *)c->bufs[B_TEXT].p;
-    unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 4));
-    unsigned *isa = (unsigned *)buf(c, B_ISA, sizeof(unsigned) * (size_t)(n + 4));
-    c->sa_rounds = 0;
-    c->lcp_from_keys = false;
-    c->sa_device_built = false;
-    c->raw_from_round0 = false;
-    c->patch_slots = 0;
-    if (n <= 0) return;
     // alphabet -> order-preserving codes 0..sigma-1 (presence of each byte value)
     unsigned *present = (unsigned *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * 256);
     RS_CUDA(cudaMemsetAsync(present, 0, sizeof(unsigned) * 8, c->stream));
@@ -765,6 +762,28 @@ void build_suffix_array(rs_ctx *c, long long n) {
     }
     c->sa_key_symbols = K;
 
+    const long long words = (n * bits + 63) / 64 + 4;
+    u64 *stream = (u64 *)buf(c, B_PACKED, sizeof(u64) * (size_t)words);
+    RS_LAUNCH_B(c, (double)n + 8.0 * words, k_pack_text, grid_for(words, 256), 256, 0, text, n, ct, bits, words,
+                stream);
+    c->packed_bits = bits;
+    return TextPrep{stream, words, bits, K, sigma};
+}
+
+void ensure_isa(rs_ctx *c);
+
+void build_suffix_array(rs_ctx *c, long long n) {
+    unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 4));
+    unsigned *isa = (unsigned *)buf(c, B_ISA, sizeof(unsigned) * (size_t)(n + 4));
+    c->sa_rounds = 0;
+    c->lcp_from_keys = false;
+    c->sa_device_built = false;
+    c->raw_from_round0 = false;
+    c->patch_slots = 0;
+    if (n <= 0) return;
+    const TextPrep tp = prepare_text(c, n);
+    const int bits = tp.bits, K = tp.K;
+    u64 *stream = tp.stream;
     u64 *k0 = (u64 *)buf(c, B_KEYS0, sizeof(u64) * (size_t)n + 16);
     u64 *k1 = (u64 *)buf(c, B_KEYS1, sizeof(u64) * (size_t)n + 16);
     unsigned *v0 = (unsigned *)buf(c, B_VALS0, sizeof(unsigned) * (size_t)n);
@@ -781,13 +800,6 @@ void build_suffix_array(rs_ctx *c, long long n) {
     unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots(n));
     RS_CUDA(cudaMemsetAsync(raw, 0, sizeof(unsigned), c->stream));
 
-    // pack the text once (n*b/8 bytes, L2-resident at 256 Mi DNA); the sort's
-    // histogram and first pass generate (key, suffix) pairs from it directly.
-    const long long words = (n * bits + 63) / 64 + 4;
-    u64 *stream = (u64 *)buf(c, B_PACKED, sizeof(u64) * (size_t)words);
-    RS_LAUNCH_B(c, (double)n + 8.0 * words, k_pack_text, grid_for(words, 256), 256, 0, text, n, ct, bits, words,
-                stream);
-    c->packed_bits = bits;
     const TextKeys tk{stream, n, bits, K, std::min<long long>(K - 1, n)};
     // round-0 keys of <= 32 bits (DNA) travel as u32: 8 instead of 12 bytes per pair and pass
     const bool key32 = bits * K <= 32;
@@ -802,6 +814,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
     long long U = n;
     const unsigned *P = nullptr;
     long long depth = K;
+    const SegBoundary sb_whole{n, 0, 0};
     c->isa_lazy = false;
     while (true) {
         ++c->sa_rounds;
@@ -830,20 +843,20 @@ void build_suffix_array(rs_ctx *c, long long n) {
         // reduce-then-scan instead of a look-back: the heavy pass never waits
         if (ks32) {
             RS_LAUNCH_B(c, 4.0 * U, (k_update<true, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa, Pa,
-                        Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
+                        Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
             tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
             // round 0: 8 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
             RS_LAUNCH_B(c, 28.0 * U, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa,
-                        Pa, Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be);
+                        Pa, Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
             ks32 = nullptr;
         } else {
             RS_LAUNCH_B(c, 8.0 * U, (k_update<true, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha,
-                        Va, tagg, tpre, lcp_d, bits, bits * K, be);
+                        Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
             tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
             RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa,
-                        isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be);
+                        isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be, sb_whole);
         }
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
