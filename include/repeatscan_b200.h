@@ -183,6 +183,9 @@ int rs_summarize_steps(rs_ctx *ctx, const int64_t *steps, int64_t count, int64_t
 #define RS_BUF_OUT0 1  /* int64 */
 #define RS_BUF_OUT1 2  /* int64 */
 #define RS_BUF_FLAT 3  /* int64 */
+#define RS_BUF_TEXT 4  /* uint8 text (n + 128 bytes; rs_set_text_device) */
+#define RS_BUF_SEND 5  /* distributed sort: (position, raw) uint32 pairs bound for other ranks */
+#define RS_BUF_RAW 6   /* distributed sort: this rank's raw LLR shard incl. its left halo */
 /* Ensure >= bytes of device buffer `which` and return its device pointer. */
 int rs_device_buffer(rs_ctx *ctx, int which, int64_t bytes, void **ptr);
 /* Declare that RS_BUF_LLRC holds m valid entries of a text of length n
@@ -195,6 +198,39 @@ int rs_query_shard(rs_ctx *ctx, int mode, int64_t lo, int64_t hi, int64_t *total
 int rs_shard_rebase(rs_ctx *ctx, int64_t base);
 /* D2H of the shard results (a, b, flat as described above). */
 int rs_fetch_shard(rs_ctx *ctx, int mode, int64_t *a, int64_t *b, int64_t *flat);
+
+/* ---- distributed suffix sort ------------------------------
+ * Replaces the serial suffix sort of suffixes.py:31-66 when it is split over
+ * `world` ranks: every rank holds the whole text (rs_set_text, or
+ * rs_device_buffer(RS_BUF_TEXT) + NCCL broadcast + rs_set_text_device) and
+ * sorts the suffixes whose top round-0 key digit falls in its range (ranges
+ * balanced on the digit histogram), i.e. one contiguous segment of the SA.
+ * Raw LLR leaves in text order through an all-to-all of (position, raw)
+ * pairs into bucket-aligned position shards, each rank then scans its shard
+ * (left halo of `halo` raw values received from the previous rank).
+ * Supported regime: 32-bit symbol-aligned round-0 keys and tied groups of at
+ * most 8 suffixes (i.i.d.-like text); info[0] = 0 otherwise and the caller
+ * runs the single-GPU path.
+ *   rs_dist_sort   info[16]: [ok, m, S (first SA slot), first key, first
+ *                  suffix, last key, last suffix, bits, K]
+ *   rs_dist_update nbr[6] = prev rank's (last key, last suffix, has_prev),
+ *                  next rank's (first key, first suffix, has_next);
+ *                  send_counts[world] = entries of RS_BUF_SEND per destination
+ *                  (concatenated in rank order); info[0] = ok, info[1] = total
+ *   rs_dist_apply  recv = device array of `count` (position, raw) uint32 pairs;
+ *                  halo_cap = halo slots reserved before the shard;
+ *                  info = [ok, P0, P1 (0-based shard), max raw, R0]; the
+ *                  shard's raw array (RS_BUF_RAW) holds raw[i] at [i - R0]
+ *   rs_dist_scan   all-ties / leftmost scan of the shard, outputs as
+ *                  rs_query_shard (rebase / fetch with rs_shard_rebase,
+ *                  rs_fetch_shard). */
+int rs_set_text_device(rs_ctx *ctx, int64_t n);
+int rs_dist_sort(rs_ctx *ctx, int32_t rank, int32_t world, int64_t *info);
+int rs_dist_update(rs_ctx *ctx, int32_t rank, int32_t world, const int64_t *nbr, int64_t *send_counts,
+                   int64_t *info);
+int rs_dist_apply(rs_ctx *ctx, int32_t rank, int32_t world, const void *recv, int64_t count, int64_t halo_cap,
+                  int64_t *info);
+int rs_dist_scan(rs_ctx *ctx, int mode, int64_t halo, int64_t *total);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,7 @@ RS_OK, RS_EINVAL, RS_ERANGE, RS_ENOMEM, RS_ECUDA, RS_ENCCL, RS_ESTATE = 0, -1, -
 MODE = {"leftmost": 0, "all": 1}
 PATH = {"raw": 0, "compact": 1}
 STAGES = ("h2d", "sa", "lcp", "raw_llr", "compact", "query", "d2h")
-BUF_LLRC, BUF_OUT0, BUF_OUT1, BUF_FLAT = 0, 1, 2, 3
+BUF_LLRC, BUF_OUT0, BUF_OUT1, BUF_FLAT, BUF_TEXT, BUF_SEND, BUF_RAW = 0, 1, 2, 3, 4, 5, 6
 
 _I64P = ctypes.POINTER(ctypes.c_int64)
 _U8P = ctypes.POINTER(ctypes.c_uint8)
@@ -78,6 +78,11 @@ SIGNATURES = {
     "rs_device_buffer": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(_VP)],
     "rs_set_compact_device": [_CTX, ctypes.c_int64, ctypes.c_int64],
     "rs_stream": [_CTX, ctypes.POINTER(_VP)],
+    "rs_set_text_device": [_CTX, ctypes.c_int64],
+    "rs_dist_sort": [_CTX, ctypes.c_int32, ctypes.c_int32, _I64P],
+    "rs_dist_update": [_CTX, ctypes.c_int32, ctypes.c_int32, _I64P, _I64P, _I64P],
+    "rs_dist_apply": [_CTX, ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int64, ctypes.c_int64, _I64P],
+    "rs_dist_scan": [_CTX, ctypes.c_int, ctypes.c_int64, _I64P],
     "rs_query_shard": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _I64P],
     "rs_shard_rebase": [_CTX, ctypes.c_int64],
     "rs_fetch_shard": [_CTX, ctypes.c_int, _I64P, _I64P, _I64P],

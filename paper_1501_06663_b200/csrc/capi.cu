@@ -29,8 +29,14 @@ long long serialize_tsv(rs_ctx *c, int mode, long long lo, long long hi);
 void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned long long *acc_host);
 void summarize(rs_ctx *c, const long long *d_steps, long long count, unsigned long long *acc_host);
 void ensure_isa(rs_ctx *c);
+void dist_sort(rs_ctx *c, long long n, int rank, int world, long long *info);
+void dist_update(rs_ctx *c, long long n, int rank, int world, const long long *nbr, long long *send_counts,
+                 long long *info);
+void dist_apply(rs_ctx *c, long long n, int rank, int world, const void *recv, long long cnt, long long hcap,
+                long long *info);
+void dist_scan(rs_ctx *c, long long n, int mode, long long halo, long long *total);
 bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
-                 long long kb, long long ke, int out_off, long long n_slots);
+                 long long kb, long long ke, int out_off, long long n_slots, long long min_lo = 1);
 
 void fail(int code, const std::string &msg) { throw RsError{code, msg}; }
 
@@ -856,9 +862,9 @@ int rs_summarize_steps(rs_ctx *c, const int64_t *steps, int64_t count, int64_t *
 
 int rs_device_buffer(rs_ctx *c, int which, int64_t bytes, void **ptr) {
     return guarded(c, [&] {
-        static const BufId ids[4] = {B_LLRC, B_OUT0, B_OUT1, B_FLAT};
-        if (which < 0 || which > 3 || bytes < 0 || !ptr) fail(RS_EINVAL, "bad buffer request");
-        *ptr = buf(c, ids[which], (size_t)bytes + 64);
+        static const BufId ids[7] = {B_LLRC, B_OUT0, B_OUT1, B_FLAT, B_TEXT, B_SEND, B_RAW};
+        if (which < 0 || which > 6 || bytes < 0 || !ptr) fail(RS_EINVAL, "bad buffer request");
+        *ptr = buf(c, ids[which], (size_t)bytes + 64 + (which == RS_BUF_TEXT ? 128 : 0));
     });
 }
 
@@ -926,6 +932,68 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
         d2h(c, b, c->bufs[B_OUT1].p, 8 * (size_t)(mode == RS_MODE_ALL ? cnt + 1 : cnt));
         if (mode == RS_MODE_ALL) d2h(c, flat, c->bufs[B_FLAT].p, 8 * (size_t)c->total);
         RS_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int rs_set_text_device(rs_ctx *c, int64_t n) {
+    return guarded(c, [&] {
+        check_n(n);
+        if (c->bufs[B_TEXT].cap < (size_t)n + 128) fail(RS_ESTATE, "text buffer too small (rs_device_buffer(RS_BUF_TEXT))");
+        unsigned char *d = (unsigned char *)c->bufs[B_TEXT].p;
+        invalidate(c);
+        RS_CUDA(cudaMemsetAsync(d + n, 0, 128, c->stream));
+        RS_CUDA(cudaStreamSynchronize(c->stream));
+        c->n = n;
+        c->have_text = true;
+    });
+}
+
+int rs_dist_sort(rs_ctx *c, int32_t rank, int32_t world, int64_t *info) {
+    return guarded(c, [&] {
+        if (!c->have_text) fail(RS_ESTATE, "no text loaded");
+        if (!info) fail(RS_EINVAL, "info is required");
+        long long tmp[16];
+        dist_sort(c, c->n, rank, world, tmp);
+        for (int i = 0; i < 16; ++i) info[i] = tmp[i];
+    });
+}
+
+int rs_dist_update(rs_ctx *c, int32_t rank, int32_t world, const int64_t *nbr, int64_t *send_counts,
+                   int64_t *info) {
+    return guarded(c, [&] {
+        if (!nbr || !send_counts || !info || world < 1) fail(RS_EINVAL, "bad arguments");
+        long long nb[6], tmp[16];
+        for (int i = 0; i < 6; ++i) nb[i] = nbr[i];
+        std::vector<long long> sc((size_t)world, 0);
+        dist_update(c, c->n, rank, world, nb, sc.data(), tmp);
+        for (int q = 0; q < world; ++q) send_counts[q] = sc[(size_t)q];
+        for (int i = 0; i < 16; ++i) info[i] = tmp[i];
+    });
+}
+
+int rs_dist_apply(rs_ctx *c, int32_t rank, int32_t world, const void *recv, int64_t count, int64_t halo_cap,
+                  int64_t *info) {
+    return guarded(c, [&] {
+        if ((count > 0 && !recv) || !info || count < 0 || halo_cap < 8) fail(RS_EINVAL, "bad arguments");
+        long long tmp[16];
+        dist_apply(c, c->n, rank, world, recv, count, halo_cap, tmp);
+        for (int i = 0; i < 16; ++i) info[i] = tmp[i];
+    });
+}
+
+int rs_dist_scan(rs_ctx *c, int mode, int64_t halo, int64_t *total) {
+    return guarded(c, [&] {
+        if (mode != RS_MODE_LEFTMOST && mode != RS_MODE_ALL) fail(RS_EINVAL, "unknown mode");
+        if (!total) fail(RS_EINVAL, "total is required");
+        bool used[RS_NUM_STAGES] = {};
+        long long t = 0;
+        {
+            Stage st(c, RS_STAGE_QUERY);
+            used[RS_STAGE_QUERY] = true;
+            dist_scan(c, c->n, mode, halo, &t);
+        }
+        collect_stages(c, used);
+        *total = t;
     });
 }
 

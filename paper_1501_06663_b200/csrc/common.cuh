@@ -68,6 +68,7 @@ enum BufId {
     B_H1,
     B_V0,
     B_V1,
+    B_SEND,      // distributed sort: (position, raw) entries bound for other ranks
     B_COUNT
 };
 
@@ -101,6 +102,14 @@ struct rs_ctx {
     long long total = 0;    // tie total of the last all-ties query
     int sa_rounds = 0;      // prefix-doubling rounds of the last SA build
     long long shard_lo = 0, shard_hi = 0;
+    // distributed suffix sort state (one rank's segment; suffix_array.cu dist_*)
+    struct {
+        long long m = 0, S = 0, P0 = 0, P1 = 0, R0 = 0, hcap = 0, send_total = 0;
+        unsigned *keys = nullptr, *vals = nullptr;
+        unsigned long long first_key = 0, last_key = 0;
+        unsigned first_pos = 0, last_pos = 0;
+        int bits = 0, K = 0, stage = 0;  // stage: 1 sorted, 2 updated, 3 applied
+    } dist;
     int sa_key_symbols = 0;                 // K of the round-0 keys
     int packed_bits = 0;                    // B_PACKED holds the current text at this many bits/symbol (0: none)
     bool isa_lazy = false;                  // B_ISA not built (device SA without later rounds): fill from SA on demand
@@ -379,6 +388,8 @@ __device__ __forceinline__ u64 text_key(const TextKeys &tk, long long p) {
 __device__ __forceinline__ long long text_pos(const TextKeys &tk, long long e) {
     return e < tk.S ? tk.n - 1 - e : e - tk.S;
 }
+bool text_digit_histograms(rs_ctx *c, const TextKeys &tk, int bits, std::vector<unsigned long long> &h);
+
 // Text prepared for the suffix sort (suffix_array.cu prepare_text).
 struct TextPrep {
     u64 *stream;      // B_PACKED: b-bit codes, zero padded

@@ -379,6 +379,30 @@ void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, uns
     *vals_out = vin;
 }
 
+// All digit histograms of the round-0 text keys (symbol-aligned digits only:
+// counted from the packed stream + shifted), copied to the host.  False when
+// the digits are not symbol-aligned.
+bool text_digit_histograms(rs_ctx *c, const TextKeys &tk, int bits, std::vector<unsigned long long> &h) {
+    const int passes = (bits + 7) / 8;
+    const long long count = tk.n;
+    if (!((8 % tk.b) == 0 && (tk.b * tk.K) % 8 == 0 && tk.b * tk.K == bits && count > (long long)passes * (8 / tk.b)))
+        return false;
+    unsigned long long *hist = (unsigned long long *)buf(c, B_HIST, sizeof(unsigned long long) * 8 * kRadix);
+    RS_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 8 * kRadix, c->stream));
+    const long long words = (count * tk.b + 63) / 64;
+    const unsigned hb = (unsigned)std::max<long long>(1, std::min<long long>((words + kNT - 1) / kNT, c->sm_count * 8));
+    switch (tk.b) {
+        case 1: RS_LAUNCH_NB(c, "k_hist_digit0", count / 8.0, k_hist_digit0<1>, hb, kNT, 0, tk, hist); break;
+        case 2: RS_LAUNCH_NB(c, "k_hist_digit0", count / 4.0, k_hist_digit0<2>, hb, kNT, 0, tk, hist); break;
+        case 4: RS_LAUNCH_NB(c, "k_hist_digit0", count / 2.0, k_hist_digit0<4>, hb, kNT, 0, tk, hist); break;
+        default: RS_LAUNCH_NB(c, "k_hist_digit0", 1.0 * count, k_hist_digit0<8>, hb, kNT, 0, tk, hist); break;
+    }
+    if (passes > 1) RS_LAUNCH(c, k_hist_shift, 1, kRadix, 0, hist, passes, 8 / tk.b, tk);
+    h.assign((size_t)passes * kRadix, 0);
+    fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
+    return true;
+}
+
 template void radix_sort_pairs<unsigned>(rs_ctx *, unsigned *, unsigned *, unsigned *, unsigned *, long long, int,
                                          unsigned **, unsigned **, const TextKeys *);
 template void radix_sort_pairs<u64>(rs_ctx *, u64 *, u64 *, unsigned *, unsigned *, long long, int, u64 **,

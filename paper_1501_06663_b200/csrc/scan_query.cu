@@ -88,7 +88,8 @@ struct Cand {
 //          hi = klast + 1 (window indices are text indices).
 template <bool RAW>
 __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict__ raw, long long count,
-                         long long kb, long long ke, long long tiles, long long *__restrict__ bounds) {
+                         long long kb, long long ke, long long tiles, long long *__restrict__ bounds,
+                         long long min_lo) {
     long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (g >= tiles) return;
     long long kfirst = kb + g * kG;
@@ -96,7 +97,9 @@ __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict
     if (klast > ke) klast = ke;
     long long lo, hi;
     if (RAW) {
-        long long a = 1, b = kfirst + 1;  // search in [1, kfirst]; answer kfirst+1 if none
+        // search in [min_lo, kfirst]; answer kfirst+1 if none (min_lo > 1: a
+        // shard's raw array starts there -- it is below every covering start)
+        long long a = min_lo > 1 ? min_lo : 1, b = kfirst + 1;
         while (a < b) {
             long long mid = (a + b) >> 1;
             if (mid + (long long)__ldg(raw + mid) - 1 >= kfirst) b = mid; else a = mid + 1;
@@ -613,7 +616,7 @@ __global__ void k_summarize(const long long *__restrict__ steps, long long n, un
 // Run the scan for positions [kb, ke] over candidates (compact entries or raw),
 // writing into B_OUT0/B_OUT1/B_FLAT.  out_off: 1 = reference layout.
 bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
-                 long long kb, long long ke, int out_off, long long n_slots) {
+                 long long kb, long long ke, int out_off, long long n_slots, long long min_lo) {
     const bool all = mode == RS_MODE_ALL;
     // compact path without a materialised LLRc: compaction fused into the scan
     const bool fused = path == RS_PATH_COMPACT && d_e == nullptr;
@@ -623,9 +626,9 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     long long tiles = (npos + kG - 1) / kG;
     long long *bounds = (long long *)buf(c, B_BOUNDS, sizeof(long long) * 2 * (size_t)tiles);
     if (rawp || fused)
-        RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds);
+        RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds, min_lo);
     else
-        RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds);
+        RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, kb, ke, tiles, bounds, 1ll);
     if (fused) {
         unsigned long long *span = (unsigned long long *)buf(c, B_SMALL, 4096) + 6;
         RS_CUDA(cudaMemsetAsync(span, 0, sizeof(*span), c->stream));
@@ -721,10 +724,10 @@ void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned l
         }
         const int sm = kStageBytes + 2 * 4 * kG;
         if (rawp) {
-            RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds);
+            RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds, 1ll);
             RS_LAUNCH(c, k_steps<true>, (unsigned)tiles, kNT, sm, d_e, d_raw, 1, n, bounds, d_steps, acc);
         } else {
-            RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds);
+            RS_LAUNCH(c, k_bounds<false>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds, 1ll);
             RS_LAUNCH(c, k_steps<false>, (unsigned)tiles, kNT, sm, d_e, d_raw, 1, n, bounds, d_steps, acc);
         }
     }

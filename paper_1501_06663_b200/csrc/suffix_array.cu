@@ -631,6 +631,114 @@ __global__ void __launch_bounds__(kSGNT) k_small_groups(const unsigned *__restri
     bucket_emit<kSGNT, 1>(be, &d, &vl, s_emit);
 }
 
+// Distributed-segment variant of k_small_groups: no direct raw stores at all
+// (a rank holds no global raw array).  keep[t] = 1 marks entries of groups left to
+// the doubling rounds.  Raw LLR (text order, random) leaves through the
+// bucketed scatter: each member's (suffix, raw) is handed to its own entry's
+// thread in shared memory and the block emits them together; a group that
+// began in the previous block is re-sorted by this block's first thread for
+// its members here (identical result), so no member is ever stored directly.
+
+__global__ void __launch_bounds__(kSGNT) k_small_groups_seg(const unsigned *__restrict__ P,
+                                                        const unsigned *__restrict__ H,
+                                                        const unsigned *__restrict__ V, long long U,
+                                                        const u64 *__restrict__ stream, int b, long long n,
+                                                        long long K, unsigned *__restrict__ sa,
+                                                        unsigned *__restrict__ isa, unsigned *__restrict__ lcp_d,
+                                                        unsigned *__restrict__ keep, BucketEmit be) {
+    __shared__ EmitSmem<kSGNT, 1> s_emit;
+    __shared__ unsigned s_dest[kSGNT], s_val[kSGNT];
+    const long long tb = blockIdx.x * (long long)kSGNT;
+    const long long t = tb + threadIdx.x;
+    s_dest[threadIdx.x] = kNoDest;
+    __syncthreads();
+    if (t < U) {
+        const unsigned head = H[t];
+        int back = 0, fwd = 0;
+        while (back < kSmallGroup && t - back - 1 >= 0 && H[t - back - 1] == head) ++back;
+        while (fwd < kSmallGroup && t + fwd + 1 < U && H[t + fwd + 1] == head) ++fwd;
+        const bool small = back + fwd + 1 <= kSmallGroup;
+        keep[t] = small ? 0u : 1u;
+        if (!small) {  // left to the doubling rounds: round-0 raw candidate (unknown LCPs as 0)
+            const unsigned slot = P[t];
+            unsigned a = lcp_d[slot], c2 = lcp_d[slot + 1];
+            a = a == kLcpUnknown ? 0u : a;
+            c2 = c2 == kLcpUnknown ? 0u : c2;
+            s_dest[threadIdx.x] = V[t];
+            s_val[threadIdx.x] = a > c2 ? a : c2;
+        }
+        const bool starter = small && back == 0;
+        if (starter || (small && back > 0 && t == tb)) {
+            const long long g0 = t - back;  // first entry of the group
+            const int s = back + fwd + 1;
+            const unsigned lb = lcp_d[head];  // group boundaries: keys differ there, LCP known from round 0
+            const unsigned le = lcp_d[head + s];
+            if (s == 2) {  // the common case, in registers
+                unsigned x = V[g0], y = V[g0 + 1], l;
+                const bool moved = suffix_less(stream, b, n, K, y, x, l);
+                if (moved) {
+                    const unsigned z = x;
+                    x = y;
+                    y = z;
+                }
+                if (starter) {  // round 0 left the pair in input order, ISA = head for both
+                    if (moved) {
+                        sa[head] = x;
+                        sa[head + 1] = y;
+                        if (isa) isa[x] = head;
+                    }
+                    if (isa) isa[y] = head + 1;
+                    lcp_d[head + 1] = l;
+                }
+                if (g0 >= tb) {
+                    s_dest[g0 - tb] = x;
+                    s_val[g0 - tb] = lb > l ? lb : l;
+                }
+                if (g0 + 1 < tb + kSGNT) {
+                    s_dest[g0 + 1 - tb] = y;
+                    s_val[g0 + 1 - tb] = l > le ? l : le;
+                }
+            } else {
+                unsigned v[kSmallGroup];
+                unsigned lc[kSmallGroup + 1];
+                lc[0] = lb;
+                lc[s] = le;
+                for (int j = 0; j < s; ++j) v[j] = V[g0 + j];
+                unsigned l;
+                for (int i = 1; i < s; ++i) {  // insertion sort by suffix comparison
+                    const unsigned x = v[i];
+                    int j = i;
+                    while (j > 0 && suffix_less(stream, b, n, K, x, v[j - 1], l)) {
+                        v[j] = v[j - 1];
+                        --j;
+                    }
+                    v[j] = x;
+                }
+                for (int j = 1; j < s; ++j) {
+                    suffix_less(stream, b, n, K, v[j - 1], v[j], l);
+                    lc[j] = l;
+                }
+                for (int j = 0; j < s; ++j) {
+                    if (starter) {
+                        const unsigned slot = head + j;
+                        sa[slot] = v[j];
+                        if (isa) isa[v[j]] = slot;
+                        if (j) lcp_d[slot] = lc[j];
+                    }
+                    const long long e = g0 + j;
+                    if (e >= tb && e < tb + kSGNT) {
+                        s_dest[e - tb] = v[j];
+                        s_val[e - tb] = lc[j] > lc[j + 1] ? lc[j] : lc[j + 1];
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const unsigned d = s_dest[threadIdx.x], vl = s_val[threadIdx.x];
+    bucket_emit<kSGNT, 1>(be, &d, &vl, s_emit);
+}
+
 // Order-preserving compaction of the (slot, head, suffix) lists to the kept
 // entries: block scan + decoupled look-back, one pass.
 constexpr int kKNT = 256, kKIPT = 8, kKTile = kKNT * kKIPT;
@@ -723,6 +831,88 @@ __global__ void k_lcp_gather(const unsigned *__restrict__ sa, const unsigned *__
     long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (r > n + 1) return;
     lcp_d[r] = (r == 0 || r >= n) ? 0u : plcp[sa[r]];
+}
+
+// ---- distributed suffix sort -------------------------------
+// Order-preserving filter of the round-0 (key, suffix) pairs, in sort input
+// order, whose top key digit lies in [dlo, dhi): one rank's share of the
+// suffixes (MSD split by the top digit).  Block scan + decoupled look-back.
+constexpr int kFNT = 256, kFIPT = 8, kFTile = kFNT * kFIPT;
+__global__ void __launch_bounds__(kFNT) k_filter_keys(TextKeys tk, long long count, int top_shift, unsigned dlo,
+                                                      unsigned dhi, unsigned *__restrict__ keys,
+                                                      unsigned *__restrict__ vals, unsigned long long *total,
+                                                      unsigned *counter, u64 *status, long long tiles) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned s_warp[kFNT / 32];
+    __shared__ u64 s_base;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const long long tile = s_tile;
+    const long long e0 = tile * kFTile + (long long)threadIdx.x * kFIPT;
+    unsigned k[kFIPT], v[kFIPT], flags = 0, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kFIPT; ++j) {
+        const long long e = e0 + j;
+        bool f = false;
+        if (e < count) {
+            const long long pos = text_pos(tk, e);
+            k[j] = (unsigned)text_key(tk, pos);
+            v[j] = (unsigned)pos;
+            const unsigned d = (k[j] >> top_shift) & 0xffu;
+            f = d >= dlo && d < dhi;
+        }
+        flags |= (unsigned)f << j;
+        cnt += f;
+    }
+    unsigned excl;
+    const unsigned tot = block_exclusive_sum<kFNT>(cnt, excl, s_warp);
+    if (threadIdx.x < 32) {
+        const u64 base = lookback_warp(status, tile, (u64)tot, OpSum());
+        if (threadIdx.x == 0) {
+            s_base = base;
+            if (tile == tiles - 1) *total = base + tot;
+        }
+    }
+    __syncthreads();
+    u64 o = s_base + excl;
+#pragma unroll
+    for (int j = 0; j < kFIPT; ++j) {
+        if (flags >> j & 1) {
+            keys[o] = k[j];
+            vals[o] = v[j];
+            ++o;
+        }
+    }
+}
+
+// The staged (position, raw) entries of each bucket, concatenated in bucket
+// order (= destination-rank order) into the send buffer.
+__global__ void k_pack_send(const uint2 *__restrict__ stage, const unsigned *__restrict__ cursor, int shift,
+                            const long long *__restrict__ off, uint2 *__restrict__ send) {
+    const long long b = blockIdx.x;
+    const unsigned cnt = cursor[b * kCursorStride];
+    const uint2 *src = stage + (b << shift);
+    uint2 *dst = send + off[b];
+    for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+}
+
+// Received (position, raw) entries -> this rank's raw shard (raw[i] at
+// rawbuf[i - R0]); max raw for the halo width.
+__global__ void k_apply_recv(const uint2 *__restrict__ recv, long long cnt, long long R0, unsigned *__restrict__ rawbuf,
+                             unsigned *maxraw) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    unsigned v = 0;
+    if (i < cnt) {
+        const uint2 e = recv[i];
+        rawbuf[(long long)e.x + 1 - R0] = e.y;
+        v = e.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = v > y ? v : y;
+    }
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(maxraw, v);
 }
 
 }  // namespace
@@ -971,6 +1161,247 @@ void build_lcp(rs_ctx *c, long long n) {
     } else {
         RS_LAUNCH_B(c, 12.0 * n, k_lcp_gather, grid_for(n + 2, 256), 256, 0, sa, plcp, n, lcp_d);
     }
+}
+
+
+// ---- distributed suffix sort: host side ---------------------------------
+// Rank r of `world` owns the suffixes whose top round-0 key digit falls in its
+// range (ranges balanced on the digit histogram every rank computes from its
+// copy of the text), i.e. one contiguous segment [S, S + m) of the suffix
+// array; the text-order outputs (raw LLR, then the query) are split into
+// bucket-aligned position shards.  Only the i.i.d.-like regime is
+// distributed: 32-bit symbol-aligned round-0 keys and tied groups of at most
+// kSmallGroup suffixes; otherwise the caller runs the single-GPU path.
+
+static unsigned host_key_lcp(unsigned long long a, unsigned long long b, int code_bits, int key_bits, unsigned K,
+                             unsigned rem_a, unsigned rem_b) {
+    const unsigned long long x = a ^ b;
+    const unsigned m = rem_a < rem_b ? rem_a : rem_b;
+    if (x) {
+        const unsigned z = (unsigned)(__builtin_clzll(x) - (64 - key_bits));
+        const unsigned l = z / (unsigned)code_bits;
+        return l < m ? l : m;
+    }
+    return m < K ? m : kLcpUnknown;
+}
+
+static void dist_buckets(long long n, int *shift, long long *nb) {
+    // the same rule as bucket_setup(c, n, ...)
+    int sh = 12;
+    while (((n + (1ll << sh) - 1) >> sh) > kMaxBuckets && sh < 30) ++sh;
+    *shift = sh;
+    *nb = std::max<long long>(1, (n + (1ll << sh) - 1) >> sh);
+}
+
+void dist_shard(long long n, int rank, int world, long long *P0, long long *P1) {
+    int shift;
+    long long nb;
+    dist_buckets(n, &shift, &nb);
+    const long long b0 = (long long)rank * nb / world, b1 = (long long)(rank + 1) * nb / world;
+    *P0 = std::min<long long>(b0 << shift, n);
+    *P1 = std::min<long long>(b1 << shift, n);
+}
+
+void dist_sort(rs_ctx *c, long long n, int rank, int world, long long *info) {
+    for (int i = 0; i < 16; ++i) info[i] = 0;
+    c->dist.stage = 0;
+    if (n < 4096 || world < 1 || rank < 0 || rank >= world) return;
+    const TextPrep tp = prepare_text(c, n);
+    const int bits = tp.bits, K = tp.K, key_bits = bits * K;
+    if (key_bits > 32) return;
+    const TextKeys tk{tp.stream, n, bits, K, std::min<long long>(K - 1, n)};
+    std::vector<unsigned long long> h;
+    if (!text_digit_histograms(c, tk, key_bits, h)) return;
+    const int passes = (key_bits + 7) / 8, top = passes - 1;
+    unsigned long long cum[257];
+    cum[0] = 0;
+    for (int d = 0; d < 256; ++d) cum[d + 1] = cum[d] + h[(size_t)top * 256 + d];
+    auto split = [&](int r) {  // first digit whose prefix reaches r/world of the suffixes
+        if (r <= 0) return 0;
+        if (r >= world) return 256;
+        const unsigned long long target = (unsigned long long)((__int128)n * r / world);
+        int d = 0;
+        while (d < 256 && cum[d] < target) ++d;
+        return d;
+    };
+    const int dlo = split(rank), dhi = split(rank + 1);
+    const long long S = (long long)cum[dlo], m = (long long)(cum[dhi] - cum[dlo]);
+    unsigned *k0 = (unsigned *)buf(c, B_KEYS0, sizeof(unsigned) * (size_t)(m + 16));
+    unsigned *k1 = (unsigned *)buf(c, B_KEYS1, sizeof(unsigned) * (size_t)(m + 16));
+    unsigned *v0 = (unsigned *)buf(c, B_VALS0, sizeof(unsigned) * (size_t)(m + 16));
+    unsigned *v1 = (unsigned *)buf(c, B_VALS1, sizeof(unsigned) * (size_t)(m + 16));
+    unsigned long long *tot = (unsigned long long *)buf(c, B_SMALL, 4096) + 12;
+    const long long tiles = (n + kFTile - 1) / kFTile;
+    Scratch sc = scratch(c, tiles);
+    RS_LAUNCH_B(c, 0.25 * n + 8.0 * m, k_filter_keys, (unsigned)tiles, kFNT, 0, tk, n, 8 * top, (unsigned)dlo,
+                (unsigned)dhi, k0, v0, tot, sc.counter, sc.status, tiles);
+    unsigned long long got = 0;
+    fetch_small(c, &got, tot, sizeof(got));
+    if ((long long)got != m) fail(RS_ECUDA, "distributed sort: filtered count mismatch");
+    unsigned *ks = k0, *vs = v0;
+    if (m > 1) radix_sort_pairs<unsigned>(c, k0, k1, v0, v1, m, key_bits, &ks, &vs, nullptr);
+    c->dist.m = m;
+    c->dist.S = S;
+    c->dist.keys = ks;
+    c->dist.vals = vs;
+    c->dist.bits = bits;
+    c->dist.K = K;
+    if (m > 0) {
+        unsigned a[2], b2[2];
+        fetch_small(c, &a[0], ks, 4);
+        fetch_small(c, &a[1], ks + m - 1, 4);
+        fetch_small(c, &b2[0], vs, 4);
+        fetch_small(c, &b2[1], vs + m - 1, 4);
+        c->dist.first_key = a[0];
+        c->dist.last_key = a[1];
+        c->dist.first_pos = b2[0];
+        c->dist.last_pos = b2[1];
+    }
+    c->dist.stage = 1;
+    info[0] = 1;
+    info[1] = m;
+    info[2] = S;
+    info[3] = (long long)c->dist.first_key;
+    info[4] = c->dist.first_pos;
+    info[5] = (long long)c->dist.last_key;
+    info[6] = c->dist.last_pos;
+    info[7] = bits;
+    info[8] = K;
+}
+
+void dist_update(rs_ctx *c, long long n, int rank, int world, const long long *nbr, long long *send_counts,
+                 long long *info) {
+    for (int i = 0; i < 16; ++i) info[i] = 0;
+    if (c->dist.stage < 1) fail(RS_ESTATE, "rs_dist_sort first");
+    const long long m = c->dist.m;
+    const int bits = c->dist.bits, K = c->dist.K, key_bits = bits * K;
+    const u64 *stream = (const u64 *)c->bufs[B_PACKED].p;
+    BucketEmit be = bucket_setup(c, n, 0, false);
+    if (m > 0) {
+        SegBoundary sb{n, 0u, 0u};
+        if (nbr[2])
+            sb.lcp_first = host_key_lcp(c->dist.first_key, (unsigned long long)nbr[0], bits, key_bits, (unsigned)K,
+                                        (unsigned)(n - c->dist.first_pos), (unsigned)(n - nbr[1]));
+        if (nbr[5])
+            sb.lcp_last = host_key_lcp((unsigned long long)nbr[3], c->dist.last_key, bits, key_bits, (unsigned)K,
+                                       (unsigned)(n - nbr[4]), (unsigned)(n - c->dist.last_pos));
+        unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(m + 4));
+        unsigned *lcp_d = (unsigned *)buf(c, B_LCP, sizeof(unsigned) * (size_t)(m + 4));
+        RS_CUDA(cudaMemsetAsync(lcp_d + m, 0, sizeof(unsigned) * 4, c->stream));
+        unsigned *Pa = (unsigned *)buf(c, B_T0, sizeof(unsigned) * (size_t)m);
+        unsigned *Ha = (unsigned *)buf(c, B_H0, sizeof(unsigned) * (size_t)m);
+        unsigned *Va = (unsigned *)buf(c, B_V0, sizeof(unsigned) * (size_t)m);
+        unsigned long long *u_dev = (unsigned long long *)buf(c, B_SMALL, 4096) + 4;
+        const long long tiles = (m + kUTile - 1) / kUTile;
+        u64 *tagg = (u64 *)buf(c, B_BOUNDS, sizeof(u64) * 2 * (size_t)(tiles + 1));
+        u64 *tpre = tagg + tiles + 1;
+        RS_LAUNCH_B(c, 4.0 * m, (k_update<true, unsigned>), (unsigned)tiles, kUNT, 0, c->dist.keys, c->dist.vals,
+                    nullptr, m, sa, nullptr, Pa, Ha, Va, tagg, tpre, lcp_d, bits, key_bits, be, sb);
+        {
+            const long long blocks = (tiles + kTSTile - 1) / kTSTile;
+            Scratch sc = scratch(c, blocks);
+            RS_LAUNCH(c, k_tile_scan_lb, (unsigned)blocks, kTSNT, 0, tagg, tiles, tpre, u_dev, sc.counter, sc.status,
+                      blocks);
+        }
+        RS_LAUNCH_B(c, 24.0 * m, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, c->dist.keys, c->dist.vals,
+                    nullptr, m, sa, nullptr, Pa, Ha, Va, tagg, tpre, lcp_d, bits, key_bits, be, sb);
+        unsigned long long un = 0;
+        fetch_small(c, &un, u_dev, sizeof(un));
+        info[2] = (long long)un;
+        if (un > 0) {
+            unsigned *keep = (unsigned *)buf(c, B_T4, sizeof(unsigned) * (size_t)un);
+            RS_LAUNCH_B(c, 16.0 * un, k_small_groups_seg, grid_for((long long)un, kSGNT), kSGNT, 0, Pa, Ha, Va,
+                        (long long)un, stream, bits, n, (long long)K, sa, nullptr, lcp_d, keep, be);
+            unsigned long long big = 0;
+            unsigned *Pb = (unsigned *)buf(c, B_T1, sizeof(unsigned) * (size_t)un);
+            unsigned *Hb = (unsigned *)buf(c, B_H1, sizeof(unsigned) * (size_t)un);
+            unsigned *Vb = (unsigned *)buf(c, B_V1, sizeof(unsigned) * (size_t)un);
+            const long long ktiles = (un + kKTile - 1) / kKTile;
+            Scratch ks_ = scratch(c, ktiles);
+            RS_LAUNCH_B(c, 16.0 * un, k_keep_compact, (unsigned)ktiles, kKNT, 0, keep, Pa, Ha, Va, (long long)un,
+                        Pb, Hb, Vb, u_dev, ks_.counter, ks_.status, ktiles);
+            fetch_small(c, &big, u_dev, sizeof(big));
+            info[3] = (long long)big;
+            if (big > 0) return;  // groups that need doubling rounds: not distributed (info[0] = 0)
+        }
+    }
+    // per destination rank: the buckets of its position shard, in order
+    std::vector<unsigned> cur((size_t)be.nb * kCursorStride);
+    fetch_small(c, cur.data(), be.cursor, sizeof(unsigned) * cur.size());
+    std::vector<long long> off((size_t)be.nb);
+    long long acc = 0;
+    for (long long b = 0; b < be.nb; ++b) {
+        off[(size_t)b] = acc;
+        acc += cur[(size_t)b * kCursorStride];
+    }
+    for (int q = 0; q < world; ++q) {
+        const long long b0 = (long long)q * be.nb / world, b1 = (long long)(q + 1) * be.nb / world;
+        long long t = 0;
+        for (long long b = b0; b < b1; ++b) t += cur[(size_t)b * kCursorStride];
+        send_counts[q] = t;
+    }
+    uint2 *send = (uint2 *)buf(c, B_SEND, sizeof(uint2) * (size_t)(acc + 8));
+    long long *d_off = (long long *)buf(c, B_I64D, sizeof(long long) * (size_t)be.nb);
+    RS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, c->stream));
+    if (acc > 0)
+        RS_LAUNCH_B(c, 16.0 * acc, k_pack_send, (unsigned)be.nb, 256, 0, be.stage, be.cursor, be.shift, d_off, send);
+    RS_CUDA(cudaStreamSynchronize(c->stream));  // the host-side offsets must outlive the copy
+    c->dist.send_total = acc;
+    c->dist.stage = 2;
+    info[0] = 1;
+    info[1] = acc;
+}
+
+void dist_apply(rs_ctx *c, long long n, int rank, int world, const void *recv, long long cnt, long long hcap,
+                long long *info) {
+    for (int i = 0; i < 16; ++i) info[i] = 0;
+    if (c->dist.stage < 2) fail(RS_ESTATE, "rs_dist_update first");
+    long long P0, P1;
+    dist_shard(n, rank, world, &P0, &P1);
+    hcap = (hcap + 3) & ~3ll;
+    const long long R0 = P0 - hcap;  // rawbuf[i - R0] = raw[i], i >= P0 + 1 - hcap; R0 = 0 mod 4 (TMA alignment)
+    const long long len = (P1 - P0) + hcap + 64;
+    unsigned *rawbuf = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * (size_t)len);
+    RS_CUDA(cudaMemsetAsync(rawbuf, 0, sizeof(unsigned) * (size_t)len, c->stream));
+    unsigned *mx = (unsigned *)((unsigned long long *)buf(c, B_SMALL, 4096) + 14);
+    RS_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned), c->stream));
+    if (cnt > 0)
+        RS_LAUNCH_B(c, 12.0 * cnt, k_apply_recv, grid_for(cnt, 256), 256, 0, (const uint2 *)recv, cnt, R0, rawbuf, mx);
+    unsigned maxraw = 0;
+    fetch_small(c, &maxraw, mx, sizeof(maxraw));
+    c->dist.P0 = P0;
+    c->dist.P1 = P1;
+    c->dist.R0 = R0;
+    c->dist.hcap = hcap;
+    c->dist.stage = 3;
+    info[0] = 1;
+    info[1] = P0;
+    info[2] = P1;
+    info[3] = maxraw;
+    info[4] = R0;
+}
+
+bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
+                 long long kb, long long ke, int out_off, long long n_slots, long long min_lo);
+
+void dist_scan(rs_ctx *c, long long n, int mode, long long halo, long long *total) {
+    if (c->dist.stage < 3) fail(RS_ESTATE, "rs_dist_apply first");
+    if (halo < 1 || halo + 4 > c->dist.hcap) fail(RS_ERANGE, "halo exceeds the raw shard's halo capacity");
+    const long long P0 = c->dist.P0, P1 = c->dist.P1, cnt = P1 - P0;
+    long long *o1 = (long long *)buf(c, B_OUT1, 8 * (size_t)(cnt + 2));
+    buf(c, B_OUT0, 8 * (size_t)(cnt + 1));
+    RS_CUDA(cudaMemsetAsync(o1, 0, 8, c->stream));
+    c->total = 0;
+    c->out_mode = mode;
+    c->out_ref_layout = false;
+    c->shard_lo = P0 + 1;
+    c->shard_hi = P1 + 1;
+    if (cnt > 0) {
+        const unsigned *d_raw = (const unsigned *)c->bufs[B_RAW].p - c->dist.R0;
+        if (!query_range(c, mode, RS_PATH_COMPACT, nullptr, 0, d_raw, P0 + 1, P1, 0, cnt, P0 + 1 - halo))
+            fail(RS_ERANGE, "repeats too long for the distributed scan");
+    }
+    *total = mode == RS_MODE_ALL ? c->total : 0;
 }
 
 // B_ISA from the final SA when round 0 skipped it (rank for the API, Kasai).

@@ -24,6 +24,7 @@ bases, CSR assembly) are backend-agnostic so they are tested with gloo on CPU.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import time
 
@@ -342,3 +343,154 @@ def bench_main(args) -> None:
     sys.stdout.flush()
     os.dup2(json_fd, 1)
     os.close(json_fd)
+
+
+# ---------------------------------------------------------------------------------------
+# distributed suffix sort: every phase is one library call per rank
+# ---------------------------------------------------------------------------------------
+HALO_CAP = 1 << 16  # raw slots reserved before each rank's shard (max repeat length distributed)
+
+
+def dist_neighbours(infos: list) -> list:
+    """Per rank the nbr[6] argument of rs_dist_update from all ranks' rs_dist_sort
+    info: (last key, last suffix, has) of the nearest earlier non-empty segment
+    and (first key, first suffix, has) of the nearest later one."""
+    world = len(infos)
+    out = []
+    for r in range(world):
+        nb = [0, 0, 0, 0, 0, 0]
+        for p in range(r - 1, -1, -1):
+            if infos[p][1] > 0:
+                nb[0:3] = [int(infos[p][5]), int(infos[p][6]), 1]
+                break
+        for q in range(r + 1, world):
+            if infos[q][1] > 0:
+                nb[3:6] = [int(infos[q][3]), int(infos[q][4]), 1]
+                break
+        out.append(nb)
+    return out
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def dist_phase_sort(ctx, rank: int, world: int) -> np.ndarray:
+    info = np.zeros(16, np.int64)
+    ctx.call("rs_dist_sort", rank, world, _native.i64(info))
+    return info
+
+
+def dist_phase_update(ctx, rank: int, world: int, nbr) -> tuple[np.ndarray, np.ndarray]:
+    nb = _i64(nbr)
+    counts = np.zeros(world, np.int64)
+    info = np.zeros(16, np.int64)
+    ctx.call("rs_dist_update", rank, world, _native.i64(nb), _native.i64(counts), _native.i64(info))
+    return counts, info
+
+
+def dist_phase_apply(ctx, rank: int, world: int, recv_ptr: int, count: int) -> np.ndarray:
+    info = np.zeros(16, np.int64)
+    ctx.call("rs_dist_apply", rank, world, ctypes.c_void_p(recv_ptr), int(count), HALO_CAP, _native.i64(info))
+    return info
+
+
+def dist_phase_scan(ctx, mode: str, halo: int) -> int:
+    total = np.zeros(1, np.int64)
+    ctx.call("rs_dist_scan", _native.MODE[mode], int(halo), _native.i64(total))
+    return int(total[0])
+
+
+def _raw_view(ctx, apply_info, lo_raw: int, count: int, device):
+    """Torch view of raw[lo_raw, lo_raw + count) in this rank's raw shard."""
+    R0 = int(apply_info[4])
+    P0, P1 = int(apply_info[1]), int(apply_info[2])
+    length = (P1 - P0) + HALO_CAP + 64
+    v = _view(ctx, _native.BUF_RAW, length, "<u4", device)
+    return v[lo_raw - R0: lo_raw - R0 + count]
+
+
+def loopback_dist_all_positions(data: np.ndarray, world: int, mode: str = "all", device=None):
+    """The distributed suffix sort + scan with `world` ranks simulated in ONE
+    process on one GPU (one library context per rank, the all-to-all and
+    halo exchanges done as device copies): exercises every phase and the
+    exchange bookkeeping exactly as the NCCL path runs them.  Returns the
+    reference-layout numpy arrays, or None when the text is outside the
+    distributed regime."""
+    import torch
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    host = np.ascontiguousarray(data, dtype=np.uint8)
+    n = int(host.size)
+    ctxs = [_native.Context(device.index or 0) for _ in range(world)]
+    try:
+        for c in ctxs:
+            c.call("rs_set_text", _native.u8(host), n)
+        infos = [dist_phase_sort(c, r, world) for r, c in enumerate(ctxs)]
+        if any(int(i[0]) == 0 for i in infos):
+            return None
+        nbrs = dist_neighbours(infos)
+        ups = [dist_phase_update(c, r, world, nbrs[r]) for r, c in enumerate(ctxs)]
+        if any(int(u[1][0]) == 0 for u in ups):
+            return None
+        sends = []
+        for r, c in enumerate(ctxs):
+            tot = int(ups[r][1][1])
+            sends.append(_view(c, _native.BUF_SEND, tot, "<i8", device)[:tot])
+        applies = []
+        for q, c in enumerate(ctxs):
+            parts = []
+            for r in range(world):
+                counts = ups[r][0]
+                off = int(counts[:q].sum())
+                parts.append(sends[r][off:off + int(counts[q])])
+            recv = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.int64, device=device)
+            torch.cuda.synchronize(device)
+            applies.append(dist_phase_apply(c, q, world, recv.data_ptr(), recv.numel()))
+            del recv
+        halo = max(int(a[3]) for a in applies) + 2
+        if halo + 4 > HALO_CAP:
+            return None
+        for r in range(world - 1):
+            P0, P1 = int(applies[r][1]), int(applies[r][2])
+            if P1 <= P0 or int(applies[r + 1][2]) <= int(applies[r + 1][1]):
+                continue
+            lo = max(P1 + 1 - halo, 1)
+            cnt = P1 + 1 - lo
+            src = _raw_view(ctxs[r], applies[r], lo, cnt, device)
+            dst = _raw_view(ctxs[r + 1], applies[r + 1], lo, cnt, device)
+            dst.copy_(src)
+        torch.cuda.synchronize(device)
+        totals = [dist_phase_scan(c, mode, halo) for c in ctxs]
+        return _assemble_host(ctxs, applies, totals, n, mode)
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def _assemble_host(ctxs, applies, totals, n: int, mode: str):
+    """rs_fetch_shard of every rank into the reference-layout arrays."""
+    if mode == "leftmost":
+        starts = np.full(n + 1, -1, np.int64)
+        lengths = np.zeros(n + 1, np.int64)
+        for c, a in zip(ctxs, applies):
+            P0, P1 = int(a[1]), int(a[2])
+            if P1 > P0:
+                c.call("rs_fetch_shard", 0, _native.i64(starts[P0 + 1:P1 + 1]), _native.i64(lengths[P0 + 1:P1 + 1]),
+                       None)
+        return starts, lengths
+    T = int(sum(totals))
+    lengths = np.zeros(n + 1, np.int64)
+    offsets = np.zeros(n + 2, np.int64)
+    flat = np.zeros(T, np.int64)
+    base = 0
+    for c, a, t in zip(ctxs, applies, totals):
+        P0, P1 = int(a[1]), int(a[2])
+        if P1 <= P0:
+            continue
+        c.call("rs_shard_rebase", base)
+        offs = np.zeros(P1 - P0 + 1, np.int64)
+        c.call("rs_fetch_shard", 1, _native.i64(lengths[P0 + 1:P1 + 1]), _native.i64(offs),
+               _native.i64(flat[base:base + t]) if t else _native.i64(np.zeros(1, np.int64)))
+        offsets[P0 + 1:P1 + 2] = offs
+        base += t
+    return lengths, offsets, flat

@@ -346,3 +346,35 @@ def test_small_tied_groups_vs_oracle(rng):
         A = rb.all_positions(rb.Text(data), mode="all")
         assert np.array_equal(A.lengths, wl) and np.array_equal(A.offsets, wo), trial
         assert np.array_equal(A.flat_starts, wf), trial
+
+
+def test_distributed_suffix_sort_loopback():
+    # the distributed suffix sort + scan with 1..5 ranks
+    # simulated on one GPU (one context per rank, exchanges as device copies)
+    from paper_1501_06663_b200 import distributed as D
+    cases = [workloads.iid_dna(300_000, 21), workloads.iid_dna(70_000, 22)]
+    data = workloads.iid_dna(200_000, 23).copy()
+    rng = np.random.default_rng(23)
+    for c in range(6):  # a few planted copies: tied groups of 2..7 suffixes
+        src, dst = int(rng.integers(0, 90_000)), int(rng.integers(100_000, 199_000))
+        data[dst:dst + 50] = data[src:src + 50]
+    cases.append(data)
+    data = workloads.iid_dna(150_000, 24).copy()
+    data[-40:] = data[1000:1040]  # a repeat that runs into the end of the text
+    cases.append(data)
+    for ci, data in enumerate(cases):
+        wl, wo, wf = oracle.all_positions(data, mode="all")
+        ws, wln = oracle.all_positions(data, mode="leftmost")
+        for world in (1, 2, 3, 5):
+            got = D.loopback_dist_all_positions(data, world, "all")
+            assert got is not None, (ci, world)
+            assert np.array_equal(got[0], wl) and np.array_equal(got[1], wo), (ci, world)
+            assert np.array_equal(got[2], wf), (ci, world)
+        got = D.loopback_dist_all_positions(data, 4, "leftmost")
+        assert np.array_equal(got[0], ws) and np.array_equal(got[1], wln), ci
+
+
+def test_distributed_suffix_sort_declines_repetitive_text():
+    from paper_1501_06663_b200 import distributed as D
+    data = workloads.periodic_mutated(50_000, 3, period=7, rate=0.0)
+    assert D.loopback_dist_all_positions(data, 2, "all") is None
