@@ -69,12 +69,13 @@ def exchange_totals(total: int, group=None, device=None) -> list[int]:
 
 
 def gather_shards(n: int, mode: str, lo: int, hi: int, a, b, flat, total_all: int, base: int,
-                  group=None, device=None):
+                  group=None, device=None, ranges=None):
     """Assemble the reference-layout arrays on rank 0 from every rank's shard.
 
     a, b, flat are torch tensors of this rank's shard (leftmost: a=starts[cnt],
     b=lengths[cnt]; all: a=lengths[cnt], b=offsets[cnt+1] already rebased,
-    flat=tie starts[T_r]).  Returns the full torch tensors on rank 0, else None.
+    flat=tie starts[T_r]).  ranges: every rank's 1-based [lo, hi) (default:
+    shard_range).  Returns the full torch tensors on rank 0, else None.
     """
     import torch
     import torch.distributed as dist
@@ -99,7 +100,7 @@ def gather_shards(n: int, mode: str, lo: int, hi: int, a, b, flat, total_all: in
         starts[lo:hi] = a[:cnt]
         lengths[lo:hi] = b[:cnt]
         for r in range(1, world):
-            rlo, rhi = shard_range(n, world, r)
+            rlo, rhi = ranges[r] if ranges else shard_range(n, world, r)
             if rhi > rlo:
                 dist.recv(starts[rlo:rhi], src=r, group=group)
                 dist.recv(lengths[rlo:rhi], src=r, group=group)
@@ -118,7 +119,7 @@ def gather_shards(n: int, mode: str, lo: int, hi: int, a, b, flat, total_all: in
         if flat is not None and flat.numel() > 0:
             flat_all[t0:t0 + flat.numel()] = flat
     for r in range(1, world):
-        rlo, rhi = shard_range(n, world, r)
+        rlo, rhi = ranges[r] if ranges else shard_range(n, world, r)
         if rhi <= rlo:
             continue
         dist.recv(lengths[rlo:rhi], src=r, group=group)
@@ -249,16 +250,20 @@ def to_answers(out, mode: str):
 # bench (torchrun, N > 1)
 # ---------------------------------------------------------------------------------------
 def bench_main(args) -> None:
-    """torchrun bench (N > 1), strong scaling over one text (SURVEY 8(e)).
+    """torchrun bench (N > 1), strong scaling over one text.
 
-    value: device-resident step -- rank 0 holds the text in HBM and rebuilds
-    SA -> LLRc, LLRc is broadcast over NVLink, every rank scans its position
-    shard and keeps its rebased CSR shard in its own HBM (as the N = 1 step
-    keeps the whole answer); CUDA events on the library stream, max over ranks.
-    e2e: the full API-level call -- text H2D, the same path, shards gathered
-    to rank 0 over NVLink and one D2H into the reference int64 arrays.
+    value: device-resident step.  Preferred path (i.i.d.-like
+    text): every rank holds the text and sorts one segment of the suffix
+    array, raw LLR is exchanged all-to-all into position shards and every
+    rank scans its shard, keeping its CSR shard in its own HBM.  Texts
+    outside that regime: rank 0 builds SA -> LLRc, LLRc is broadcast and the
+    ranks scan position shards.  CUDA events on the library
+    stream, max over ranks.
+    e2e: the API-level call -- text from rank 0's host, the same path, shards
+    gathered to rank 0 over NVLink and one D2H into the reference int64 arrays.
     """
     import json
+    import sys
 
     import torch
     import torch.distributed as dist
@@ -267,7 +272,6 @@ def bench_main(args) -> None:
 
     # stdout carries exactly one JSON line: everything else written to fd 1
     # (e.g. the NCCL version banner at communicator creation) goes to stderr
-    import sys
     sys.stdout.flush()
     json_fd = os.dup(1)
     os.dup2(2, 1)
@@ -275,15 +279,34 @@ def bench_main(args) -> None:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
-    data = workloads.make(args.config, args.n) if rank == 0 else None
-    ctx = _native.context(local)
+    device = torch.device("cuda", local)
+    data = None
     if rank == 0:
-        host = np.ascontiguousarray(data, dtype=np.uint8)
+        gen = workloads.make(args.config, args.n)
+        data = _native.pinned_pool.empty(int(gen.size), np.uint8)  # pinned: the e2e H2D runs at PCIe rate
+        data[:] = gen
+    nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device=device)
+    dist.broadcast(nn, src=0)
+    n = int(nn.item())
+    ctx = _native.context(local)
+    # text resident on every rank (the distributed sort reads it everywhere)
+    with ctx.lock:
+        tv = _view(ctx, _native.BUF_TEXT, n, "|u1", device)[:n]
+        if rank == 0:
+            tv.copy_(torch.from_numpy(data))
+        dist.broadcast(tv, src=0)
+        torch.cuda.synchronize(device)
+        ctx.call("rs_set_text_device", n)
+    use_dist = dist_sa_all_positions(None, n, "all", resident=True, gather=False) is not None
+    if not use_dist and rank == 0:  # rank 0 keeps the text for the LLRc path
         with ctx.lock:
-            ctx.call("rs_set_text", _native.u8(host), int(host.size))
+            ctx.call("rs_set_text", _native.u8(data), n)
 
     def step():
-        sharded_all_positions(data, "all", resident=True, gather=False)
+        if use_dist:
+            dist_sa_all_positions(None, n, "all", resident=True, gather=False)
+        else:
+            sharded_all_positions(data, "all", resident=True, gather=False)
 
     for _ in range(args.warmup):
         step()
@@ -297,15 +320,12 @@ def bench_main(args) -> None:
     ctx.record(1)
     ms = ctx.elapsed_ms(0, 1) / args.steps
     launches = (ctx.launches() - l0) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device="cuda")
-    dist.broadcast(nn, src=0)
-    n = int(nn.item())
-    lt = torch.tensor([launches], dtype=torch.float64, device="cuda")
+    lt = torch.tensor([launches], dtype=torch.float64, device=device)
     dist.all_reduce(lt, op=dist.ReduceOp.SUM)
-    # e2e: H2D of the text on rank 0 (inside rs_set_text) + gather + final D2H of the CSR
+    # e2e: text H2D on rank 0 + the whole path + gather + final D2H of the CSR
     e2e = []
     res = None
     for i in range(args.warmup + max(1, args.steps)):  # warm-up fills the pinned result pool
@@ -313,7 +333,7 @@ def bench_main(args) -> None:
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = sharded_all_positions(data, "all")
+        out = (dist_sa_all_positions(data, n, "all") if use_dist else sharded_all_positions(data, "all"))
         res = to_answers(out, "all") if rank == 0 else None
         torch.cuda.synchronize()
         dist.barrier()
@@ -321,6 +341,9 @@ def bench_main(args) -> None:
             e2e.append(time.perf_counter() - t0)
     if rank == 0:
         T = int(res.flat_starts.size)
+        par = (f"distributed suffix sort x{world}: SA segments by top key digit, raw LLR all-to-all into "
+               f"position shards, per-shard scan; CSR shards stay on their GPUs" if use_dist else
+               f"position shards x{world} (SA/LLRc on rank 0, NCCL broadcast; CSR shards stay on their GPUs)")
         line = {
             "metric": "positions/sec, all-longest-repeat query, n=256M DNA, 1/2/4/8 B200 vs CPU",
             "value": n / (ms * 1e-3), "unit": "positions/s", "n_gpus": world, "steps": args.steps,
@@ -328,14 +351,14 @@ def bench_main(args) -> None:
             "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
             "data": "synthetic",
             "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
-                       "parallelism": f"position shards x{world} (SA/LLRc on rank 0, NCCL broadcast; "
-                                      "CSR shards stay on their GPUs)",
+                       "parallelism": par,
                        "l2": "input 256 MiB > 126 MB L2; all arrays rebuilt each step",
                        "T": T},
             "gpu_launches": int(round(float(lt.item()) * args.steps)),
             "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": n,
                     "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
-                    "path": "sharded_all_positions + NCCL gather to rank 0 + D2H"},
+                    "path": ("dist_sa_all_positions" if use_dist else "sharded_all_positions")
+                            + " + NCCL gather to rank 0 + D2H"},
         }
         os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
@@ -494,3 +517,115 @@ def _assemble_host(ctxs, applies, totals, n: int, mode: str):
         offsets[P0 + 1:P1 + 2] = offs
         base += t
     return lengths, offsets, flat
+
+
+def dist_shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """0-based [P0, P1) position shard of `rank` in the distributed sort
+    (bucket-aligned; the library's dist_shard / bucket_setup rule)."""
+    sh = 12
+    while (n + (1 << sh) - 1) >> sh > 256 and sh < 30:
+        sh += 1
+    nb = max(1, (n + (1 << sh) - 1) >> sh)
+    b0, b1 = rank * nb // world, (rank + 1) * nb // world
+    return min(b0 << sh, n), min(b1 << sh, n)
+
+
+def dist_sa_all_positions(data: np.ndarray | None, n: int, mode: str = "all", group=None,
+                          resident: bool = False, gather: bool = True):
+    """Distributed suffix sort + scan over the ranks of `group` (NCCL).
+
+    Every rank sorts one SA segment (MSD split by the top round-0 key digit),
+    raw LLR goes to bucket-aligned position shards by all-to-all, each rank
+    scans its shard.  resident=True: every rank already holds the text
+    (rs_set_text_device); else rank 0's `data` is broadcast over NVLink.
+    Returns rank 0's reference-layout tensors (gather=True), True on the
+    other ranks / without gather, or None everywhere when the text is outside
+    the distributed regime (long or highly repeated substrings: the caller
+    then uses sharded_all_positions).
+    """
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev_index = torch.cuda.current_device()
+    device = torch.device("cuda", dev_index)
+    ctx = _native.context(dev_index)
+    kw = dict(dtype=torch.int64, device=device)
+    with ctx.lock:
+        if not resident:
+            tv = _view(ctx, _native.BUF_TEXT, n, "|u1", device)[:n]
+            if rank == 0:
+                tv.copy_(torch.from_numpy(np.ascontiguousarray(data, dtype=np.uint8)), non_blocking=True)
+            dist.broadcast(tv, src=0, group=group)
+            torch.cuda.synchronize(device)
+            ctx.call("rs_set_text_device", n)
+        info = dist_phase_sort(ctx, rank, world)
+        allinfo = torch.zeros(world * 16, **kw)
+        dist.all_gather_into_tensor(allinfo, torch.from_numpy(info).to(device), group=group)
+        infos = allinfo.view(world, 16).cpu().numpy()
+        if (infos[:, 0] == 0).any():
+            return None
+        counts, uinfo = dist_phase_update(ctx, rank, world, dist_neighbours(list(infos))[rank])
+        ok = torch.tensor([int(uinfo[0])], **kw)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            return None
+        send_counts = torch.from_numpy(counts).to(device)
+        recv_counts = torch.empty(world, **kw)
+        dist.all_to_all_single(recv_counts, send_counts, group=group)
+        rc = [int(x) for x in recv_counts.cpu().tolist()]
+        sc = [int(x) for x in counts.tolist()]
+        total_send = int(uinfo[1])
+        send = _view(ctx, _native.BUF_SEND, max(total_send, 1), "<i8", device)[:total_send]
+        recv = torch.empty(sum(rc), **kw)
+        dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc, group=group)
+        torch.cuda.synchronize(device)
+        ainfo = dist_phase_apply(ctx, rank, world, recv.data_ptr(), recv.numel())
+        del recv
+        mx = torch.tensor([int(ainfo[3])], **kw)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        halo = int(mx.item()) + 2
+        if halo + 4 > HALO_CAP:
+            return None
+        # left halo: the last `halo` raw values of the previous non-empty shard
+        P0, P1 = int(ainfo[1]), int(ainfo[2])
+        ops = []
+        if P1 > P0 and rank + 1 < world:
+            q0, q1 = dist_shard(n, rank + 1, world)
+            if q1 > q0:
+                lo = max(P1 + 1 - halo, 1)
+                ops.append(dist.P2POp(dist.isend, _raw_view(ctx, ainfo, lo, P1 + 1 - lo, device).contiguous(),
+                                      rank + 1, group))
+        if P1 > P0 and rank > 0:
+            lo = max(P0 + 1 - halo, 1)
+            buf_in = _raw_view(ctx, ainfo, lo, P0 + 1 - lo, device)
+            ops.append(dist.P2POp(dist.irecv, buf_in, rank - 1, group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        torch.cuda.synchronize(device)
+        total = dist_phase_scan(ctx, mode, halo)
+        lo1, hi1 = P0 + 1, P1 + 1  # 1-based half-open
+        cnt = hi1 - lo1
+        if mode == "all":
+            totals = exchange_totals(total, group, device)
+            bases = tie_bases(totals)
+            if cnt > 0:
+                ctx.call("rs_shard_rebase", bases[rank])
+            T_all = sum(totals)
+        if not gather:
+            ctx.synchronize()
+            return True
+        ranges = [tuple(x + 1 for x in dist_shard(n, r, world)) for r in range(world)]
+        a = _view(ctx, _native.BUF_OUT0, max(cnt, 1), "<i8", device)
+        if mode == "all":
+            b = _view(ctx, _native.BUF_OUT1, cnt + 1, "<i8", device)
+            f = _view(ctx, _native.BUF_FLAT, total, "<i8", device)
+            ctx.synchronize()
+            out = gather_shards(n, mode, lo1, hi1, a, b, f, T_all, bases[rank], group, device, ranges=ranges)
+        else:
+            b = _view(ctx, _native.BUF_OUT1, max(cnt, 1), "<i8", device)
+            ctx.synchronize()
+            out = gather_shards(n, mode, lo1, hi1, a, b, None, 0, 0, group, device, ranges=ranges)
+        torch.cuda.synchronize(device)
+    return out if rank == 0 else True

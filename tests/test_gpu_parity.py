@@ -278,6 +278,23 @@ def test_distributed_single_rank_nccl():
         res = D.to_answers(out, "leftmost")
         ws, wln = oracle.all_positions(data, mode="leftmost")
         assert np.array_equal(res.starts, ws) and np.array_equal(res.lengths, wln)
+        # the distributed suffix sort through NCCL (text broadcast, all-to-all,
+        # halo send/recv, gather) on an i.i.d.-like text
+        data = workloads.iid_dna(300_000, 31)
+        for mode in ("all", "leftmost"):
+            out = D.dist_sa_all_positions(data, int(data.size), mode)
+            assert out is not None
+            res = D.to_answers(out, mode)
+            if mode == "all":
+                wl, wo, wf = oracle.all_positions(data, mode="all")
+                assert np.array_equal(res.lengths, wl) and np.array_equal(res.offsets, wo)
+                assert np.array_equal(res.flat_starts, wf)
+            else:
+                ws, wln = oracle.all_positions(data, mode="leftmost")
+                assert np.array_equal(res.starts, ws) and np.array_equal(res.lengths, wln)
+        # outside the distributed regime it declines (caller falls back)
+        rep = workloads.periodic_mutated(60_000, 3, period=7, rate=0.0)
+        assert D.dist_sa_all_positions(rep, int(rep.size), "all") is None
     finally:
         dist.destroy_process_group()
 
