@@ -87,3 +87,32 @@ def test_shard_ranges_partition():
                 covered += list(range(lo, hi))
             assert covered == list(range(1, n + 1))
     assert D.tie_bases([3, 0, 5]) == [0, 3, 3]
+
+
+def test_dist_shard_partition():
+    # distributed suffix sort: bucket-aligned position shards cover [0, n) exactly
+    from paper_1501_06663_b200.distributed import dist_shard
+    for n in (4096, 5000, 1 << 20, (1 << 20) + 7, 268435456, 1073741824):
+        for world in (1, 2, 3, 5, 8):
+            prev = 0
+            for r in range(world):
+                p0, p1 = dist_shard(n, r, world)
+                assert p0 == prev and p1 >= p0
+                prev = p1
+            assert prev == n
+
+
+def test_dist_neighbours():
+    from paper_1501_06663_b200.distributed import dist_neighbours
+    z = [0] * 16
+
+    def info(m, fk, fp, lk, lp):
+        i = list(z)
+        i[0], i[1], i[3], i[4], i[5], i[6] = 1, m, fk, fp, lk, lp
+        return i
+
+    infos = [info(3, 10, 100, 11, 101), info(0, 0, 0, 0, 0), info(5, 20, 200, 21, 201), info(2, 30, 300, 31, 301)]
+    nb = dist_neighbours(infos)
+    assert nb[0] == [0, 0, 0, 20, 200, 1]           # next non-empty segment is rank 2
+    assert nb[2] == [11, 101, 1, 30, 300, 1]        # previous non-empty is rank 0
+    assert nb[3] == [21, 201, 1, 0, 0, 0]
