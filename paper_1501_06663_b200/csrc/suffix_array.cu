@@ -886,33 +886,53 @@ __global__ void __launch_bounds__(kFNT) k_filter_keys(TextKeys tk, long long cou
 }
 
 // The staged (position, raw) entries of each bucket, concatenated in bucket
-// order (= destination-rank order) into the send buffer.
+// order (= destination-rank order) into the send buffer; blockIdx.x = chunk
+// of 4096 entries, blockIdx.y = bucket.
 __global__ void k_pack_send(const uint2 *__restrict__ stage, const unsigned *__restrict__ cursor, int shift,
                             const long long *__restrict__ off, uint2 *__restrict__ send) {
-    const long long b = blockIdx.x;
+    const long long b = blockIdx.y;
     const unsigned cnt = cursor[b * kCursorStride];
+    const unsigned begin = blockIdx.x * 4096u;
+    if (begin >= cnt) return;
+    const unsigned end = cnt - begin < 4096u ? cnt : begin + 4096u;
     const uint2 *src = stage + (b << shift);
     uint2 *dst = send + off[b];
-    for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+    for (unsigned i = begin + threadIdx.x; i < end; i += blockDim.x) dst[i] = src[i];
 }
 
 // Received (position, raw) entries -> this rank's raw shard (raw[i] at
-// rawbuf[i - R0]); max raw for the halo width.
-__global__ void k_apply_recv(const uint2 *__restrict__ recv, long long cnt, long long R0, unsigned *__restrict__ rawbuf,
-                             unsigned *maxraw) {
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+// rawbuf[i - R0]); max raw for the halo width (one atomic per block).
+constexpr int kARNT = 256, kARIPT = 8;
+__global__ void __launch_bounds__(kARNT) k_apply_recv(const uint2 *__restrict__ recv, long long cnt, long long R0,
+                                                      unsigned *__restrict__ rawbuf, unsigned *maxraw) {
+    __shared__ unsigned s_max[kARNT / 32];
+    const long long i0 = blockIdx.x * (long long)(kARNT * kARIPT) + threadIdx.x;
+    uint2 e[kARIPT];
+#pragma unroll
+    for (int j = 0; j < kARIPT; ++j) {  // all loads in flight before the stores
+        const long long i = i0 + (long long)j * kARNT;
+        e[j] = i < cnt ? recv[i] : make_uint2(0xffffffffu, 0u);
+    }
     unsigned v = 0;
-    if (i < cnt) {
-        const uint2 e = recv[i];
-        rawbuf[(long long)e.x + 1 - R0] = e.y;
-        v = e.y;
+#pragma unroll
+    for (int j = 0; j < kARIPT; ++j) {
+        if (e[j].x != 0xffffffffu) {
+            rawbuf[(long long)e[j].x + 1 - R0] = e[j].y;
+            v = v > e[j].y ? v : e[j].y;
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         const unsigned y = __shfl_xor_sync(0xffffffffu, v, o);
         v = v > y ? v : y;
     }
-    if ((threadIdx.x & 31) == 0 && v) atomicMax(maxraw, v);
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned m = 0;
+        for (int w = 0; w < kARNT / 32; ++w) m = m > s_max[w] ? m : s_max[w];
+        if (m) atomicMax(maxraw, m);
+    }
 }
 
 }  // namespace
@@ -1343,8 +1363,11 @@ void dist_update(rs_ctx *c, long long n, int rank, int world, const long long *n
     uint2 *send = (uint2 *)buf(c, B_SEND, sizeof(uint2) * (size_t)(acc + 8));
     long long *d_off = (long long *)buf(c, B_I64D, sizeof(long long) * (size_t)be.nb);
     RS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, c->stream));
+    unsigned maxc = 0;
+    for (long long b = 0; b < be.nb; ++b) maxc = std::max(maxc, cur[(size_t)b * kCursorStride]);
     if (acc > 0)
-        RS_LAUNCH_B(c, 16.0 * acc, k_pack_send, (unsigned)be.nb, 256, 0, be.stage, be.cursor, be.shift, d_off, send);
+        RS_LAUNCH_B(c, 16.0 * acc, k_pack_send, dim3((maxc + 4095) / 4096, (unsigned)be.nb), 256, 0, be.stage,
+                    be.cursor, be.shift, d_off, send);
     RS_CUDA(cudaStreamSynchronize(c->stream));  // the host-side offsets must outlive the copy
     c->dist.send_total = acc;
     c->dist.stage = 2;
@@ -1366,7 +1389,8 @@ void dist_apply(rs_ctx *c, long long n, int rank, int world, const void *recv, l
     unsigned *mx = (unsigned *)((unsigned long long *)buf(c, B_SMALL, 4096) + 14);
     RS_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned), c->stream));
     if (cnt > 0)
-        RS_LAUNCH_B(c, 12.0 * cnt, k_apply_recv, grid_for(cnt, 256), 256, 0, (const uint2 *)recv, cnt, R0, rawbuf, mx);
+        RS_LAUNCH_B(c, 12.0 * cnt, k_apply_recv, (unsigned)((cnt + kARNT * kARIPT - 1) / (kARNT * kARIPT)), kARNT,
+                    0, (const uint2 *)recv, cnt, R0, rawbuf, mx);
     unsigned maxraw = 0;
     fetch_small(c, &maxraw, mx, sizeof(maxraw));
     c->dist.P0 = P0;
