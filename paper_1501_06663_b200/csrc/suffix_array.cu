@@ -302,15 +302,18 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
     }
     // ---- round 0: SA slots are t itself -> each thread stores its 8 slots as
     //      two 16-byte vectors (a warp covers 1 KB contiguously) ----
+    //      (sa == null: the sorted suffix array itself becomes the SA)
     const bool full = t0 + kUIPT <= U;
-    if (full) {
-        uint4 *d = reinterpret_cast<uint4 *>(sa + t0);
-        d[0] = make_uint4(vv[0], vv[1], vv[2], vv[3]);
-        d[1] = make_uint4(vv[4], vv[5], vv[6], vv[7]);
-    } else {
+    if (sa) {
+        if (full) {
+            uint4 *d = reinterpret_cast<uint4 *>(sa + t0);
+            d[0] = make_uint4(vv[0], vv[1], vv[2], vv[3]);
+            d[1] = make_uint4(vv[4], vv[5], vv[6], vv[7]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < kUIPT; ++j)
-            if (t0 + j < U) sa[t0 + j] = vv[j];
+            for (int j = 0; j < kUIPT; ++j)
+                if (t0 + j < U) sa[t0 + j] = vv[j];
+        }
     }
     // LCP of adjacent suffixes from their packed K-symbol keys (capped by the
     // suffix lengths); kLcpUnknown (true LCP >= K) when undecided.
@@ -983,7 +986,7 @@ TextPrep prepare_text(rs_ctx *c, long long n) {
 void ensure_isa(rs_ctx *c);
 
 void build_suffix_array(rs_ctx *c, long long n) {
-    unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 4));
+    unsigned *sa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 16));  // round 0 swaps it with a vals buffer
     unsigned *isa = (unsigned *)buf(c, B_ISA, sizeof(unsigned) * (size_t)(n + 4));
     c->sa_rounds = 0;
     c->lcp_from_keys = false;
@@ -996,8 +999,8 @@ void build_suffix_array(rs_ctx *c, long long n) {
     u64 *stream = tp.stream;
     u64 *k0 = (u64 *)buf(c, B_KEYS0, sizeof(u64) * (size_t)n + 16);
     u64 *k1 = (u64 *)buf(c, B_KEYS1, sizeof(u64) * (size_t)n + 16);
-    unsigned *v0 = (unsigned *)buf(c, B_VALS0, sizeof(unsigned) * (size_t)n);
-    unsigned *v1 = (unsigned *)buf(c, B_VALS1, sizeof(unsigned) * (size_t)n);
+    unsigned *v0 = (unsigned *)buf(c, B_VALS0, sizeof(unsigned) * (size_t)(n + 16));
+    unsigned *v1 = (unsigned *)buf(c, B_VALS1, sizeof(unsigned) * (size_t)(n + 16));
     unsigned *Pa = (unsigned *)buf(c, B_T0, sizeof(unsigned) * (size_t)n);
     unsigned *Pb = (unsigned *)buf(c, B_T1, sizeof(unsigned) * (size_t)n);
     unsigned *Ha = (unsigned *)buf(c, B_H0, sizeof(unsigned) * (size_t)n);
@@ -1057,16 +1060,24 @@ void build_suffix_array(rs_ctx *c, long long n) {
             tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
             // round 0: 8 B (key, suffix) in; 4 B SA + 4 B LCP + 12 B (ISA, raw) staging out
-            RS_LAUNCH_B(c, 28.0 * U, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U, sa, isa,
-                        Pa, Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
+            RS_LAUNCH_B(c, 24.0 * U, (k_update<false, unsigned>), (unsigned)tiles, kUNT, 0, ks32, vs, P, U,
+                        (unsigned *)nullptr, isa, Pa, Ha, Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
             ks32 = nullptr;
         } else {
             RS_LAUNCH_B(c, 8.0 * U, (k_update<true, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa, isa, Pa, Ha,
                         Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
             tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
-            RS_LAUNCH_B(c, (P ? 24.0 : 32.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U, sa,
-                        isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits, bits * K, be, sb_whole);
+            RS_LAUNCH_B(c, (P ? 24.0 : 28.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U,
+                        P ? sa : (unsigned *)nullptr, isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits,
+                        bits * K, be, sb_whole);
+        }
+        if (!P) {  // round 0: the sorted suffixes are the SA -- adopt their buffer instead of copying
+            const BufId idv = (vs == (const unsigned *)c->bufs[B_VALS0].p) ? B_VALS0 : B_VALS1;
+            std::swap(c->bufs[B_SA], c->bufs[idv]);
+            sa = (unsigned *)c->bufs[B_SA].p;
+            if (idv == B_VALS0) v0 = (unsigned *)c->bufs[B_VALS0].p;
+            else v1 = (unsigned *)c->bufs[B_VALS1].p;
         }
         unsigned long long un = 0;
         fetch_small(c, &un, u_dev, sizeof(un));
