@@ -793,6 +793,20 @@ __global__ void k_phi(const unsigned *__restrict__ sa, long long n, unsigned *__
     phi[sa[j]] = j ? sa[j - 1] : kNone;
 }
 
+// PLCP[i] = lcp(i, phi[i]) from scratch, one thread per position (short LCPs).
+__global__ void k_plcp_flat(const u64 *__restrict__ stream, int b, const unsigned *__restrict__ phi, long long n,
+                            unsigned *__restrict__ plcp) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned j = phi[i];
+    if (j == kNone) {
+        plcp[i] = 0;
+        return;
+    }
+    const long long lim = n - (i > (long long)j ? i : (long long)j);
+    plcp[i] = (unsigned)packed_lcp(stream, b, i, (long long)j, 0, lim);
+}
+
 // Kasai over text-order chunks: PLCP[i] = lcp(i, phi[i]); carry h-1 within a chunk.
 __global__ void k_plcp(const unsigned char *__restrict__ text, const u64 *__restrict__ stream, int b,
                        const unsigned *__restrict__ phi, long long n, long long chunk, unsigned *__restrict__ plcp) {
@@ -1181,11 +1195,19 @@ void build_lcp(rs_ctx *c, long long n) {
         scatter_phi(c, sa, n, phi);
     else
         RS_LAUNCH_B(c, 8.0 * n, k_phi, grid_for(n, 256), 256, 0, sa, n, phi);
-    long long chunk = std::max<long long>(32, n >> 19);
-    long long chunks = (n + chunk - 1) / chunk;
     const u64 *stream = c->packed_bits ? (const u64 *)c->bufs[B_PACKED].p : nullptr;
-    RS_LAUNCH_B(c, 10.0 * n, k_plcp, grid_for(chunks, 128), 128, 0, text, stream, c->packed_bits, phi, n, chunk,
-                plcp);
+    // Short LCPs (the doubling depth bounds the longest: < 1024 symbols here):
+    // every position compares from scratch, one thread each, instead of
+    // Kasai's carried h along a sequential chunk -- far more parallelism for
+    // the same few packed-window compares.  Long repeats keep the carry.
+    if (stream && c->sa_device_built && c->sa_final_depth <= 1024) {
+        RS_LAUNCH_B(c, 8.0 * n, k_plcp_flat, grid_for(n, 256), 256, 0, stream, c->packed_bits, phi, n, plcp);
+    } else {
+        long long chunk = std::max<long long>(32, n >> 19);
+        long long chunks = (n + chunk - 1) / chunk;
+        RS_LAUNCH_B(c, 10.0 * n, k_plcp, grid_for(chunks, 128), 128, 0, text, stream, c->packed_bits, phi, n, chunk,
+                    plcp);
+    }
     if (bucketed) {
         RS_CUDA(cudaMemsetAsync(lcp_d + n, 0, sizeof(unsigned) * 2, c->stream));
         scatter_by(c, (const unsigned *)c->bufs[B_ISA].p, plcp, n, lcp_d, n);
