@@ -29,6 +29,8 @@
 // Device layouts: sa/isa u32[n] 0-based; lcp_d u32[n+2] with lcp_d[r] =
 // reference lcp[r+1] (lcp_d[0] = lcp_d[n] = 0); raw u32 1-based (raw[0] = 0).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -1105,6 +1107,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
         }
         if (!P) c->isa_lazy = skip_isa;
         U = (long long)un;
+        if (std::getenv("RS_DEBUG_ROUNDS")) std::fprintf(stderr, "round %d depth %lld unsorted %lld\n", c->sa_rounds, depth, U);
         if (c->sa_rounds == 1 && U > 0 && U <= n / 8) {  // mostly small groups (i.i.d.-like text)
             // small tied groups: final order + LCP + raw by direct comparison;
             // the lists keep only the larger groups (order preserved)
