@@ -165,7 +165,7 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8 text / int64 answers", "data": "synthetic",
         "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
                    "note": "bounded prefix of the workload per step; CPU port of the reference"},
@@ -294,7 +294,7 @@ def run_single(args) -> None:
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
         "data": "synthetic",
         "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
                    "pipeline": "SA (prefix doubling: onesweep LSD radix, small tied groups sorted "
