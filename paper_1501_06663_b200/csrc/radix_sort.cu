@@ -139,9 +139,11 @@ __device__ __forceinline__ unsigned peer_bit(unsigned peers, unsigned x, unsigne
 template <typename KeyT>
 struct SortSmem {
     union {
-        KeyT keys[kTile];  // keys in digit order, then
+        KeyT keys[kTile];  // the tile's keys (TMA), then keys in digit order, then
         unsigned vals[kTile];  // values in digit order
     } x;
+    unsigned tv[sizeof(KeyT) == 8 ? kTile : 4];  // u64 passes: the tile's values (TMA)
+    unsigned long long bar;
     unsigned short warp_cnt[kWarps][kRadix];  // per-warp digit counts, then warp offsets
     unsigned char digit[kTile];               // digit of each slot (value scatter)
     unsigned tile_start[kRadix];              // exclusive scan of tile digit counts
@@ -177,10 +179,27 @@ __global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3)
 
     KeyT k[kIPT];
     unsigned r[kIPT];
+    // u64 passes: the tile's keys and values arrive by two bulk copies (TMA),
+    // no value registers until the exchange (u32 passes measured faster with
+    // per-thread loads: 5.07 vs 5.32 ms per 3 passes at 256 Mi)
+    constexpr bool kTma = !TEXT && sizeof(KeyT) == 8;
+    if (kTma) {
+        if (threadIdx.x == 0) {
+            mbar_init(&sm.bar, 1);
+            const unsigned kb = ((unsigned)tile_count * (unsigned)sizeof(KeyT) + 15u) & ~15u;
+            const unsigned vb = ((unsigned)tile_count * 4u + 15u) & ~15u;
+            mbar_expect_tx(&sm.bar, kb + vb);
+            tma_load_1d(sm.x.keys, keys_in + tbase, kb, &sm.bar);
+            tma_load_1d(sm.tv, vals_in + tbase, vb, &sm.bar);
+        }
+        __syncthreads();
+        mbar_wait(&sm.bar, 0);
+    }
 #pragma unroll
     for (int i = 0; i < kIPT; ++i) {
         const int o = wbase + i * 32;
-        if (o < tile_count) k[i] = TEXT ? (KeyT)text_key(tk, text_pos(tk, tbase + o)) : keys_in[tbase + o];
+        if (o < tile_count)
+            k[i] = TEXT ? (KeyT)text_key(tk, text_pos(tk, tbase + o)) : kTma ? sm.x.keys[o] : keys_in[tbase + o];
     }
     // 1) tile digit histogram first, published right away (decoupled
     //    look-back: successors can use this tile's aggregate while it is still
@@ -271,7 +290,7 @@ __global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3)
         }
     }
     unsigned v[kIPT];
-    if (!TEXT) {
+    if (!TEXT && !kTma) {
 #pragma unroll
         for (int i = 0; i < kIPT; ++i)
             if (wbase + i * 32 < tile_count) v[i] = vals_in[tbase + wbase + i * 32];
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3)
 #pragma unroll
     for (int i = 0; i < kIPT; ++i) {
         const int o = wbase + i * 32;
-        if (o < tile_count) sm.x.vals[r[i]] = TEXT ? (unsigned)text_pos(tk, tbase + o) : v[i];
+        if (o < tile_count) sm.x.vals[r[i]] = TEXT ? (unsigned)text_pos(tk, tbase + o) : kTma ? sm.tv[o] : v[i];
     }
     __syncthreads();
 #pragma unroll
