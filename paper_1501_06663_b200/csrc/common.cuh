@@ -437,6 +437,7 @@ TextPrep prepare_text(rs_ctx *c, long long n);
 struct SegBoundary {
     long long n_text;
     unsigned lcp_first, lcp_last;
+    unsigned long long *group_count;  // optional: += number of still-tied groups (final pass)
 };
 
 // Sorts (keys, vals) pairs by the low `bits` bits of keys, stable.  With tk,

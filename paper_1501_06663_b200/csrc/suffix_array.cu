@@ -124,20 +124,86 @@ __global__ void k_pack_text(const unsigned char *__restrict__ text, long long n,
     stream[w] = x;
 }
 
-// Round r >= 1 keys for the unsorted slots P[0..U).
-__global__ void k_make_keys(const unsigned *__restrict__ H, const unsigned *__restrict__ V, long long U,
-                            const unsigned *__restrict__ isa, long long n, long long h,
+// Round r >= 1 keys for the unsorted slots P[0..U): (group, lo) packed as
+// group << lo_bits | lo, the group given either as its head slot or as its
+// dense ordinal (the list is in slot order, so groups are consecutive runs
+// of equal heads); both orders agree.
+__global__ void k_make_keys(const unsigned *__restrict__ G, const unsigned *__restrict__ V, long long U,
+                            const unsigned *__restrict__ isa, long long n, long long h, int lo_bits,
                             u64 *__restrict__ keys, unsigned *__restrict__ vals) {
     long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (t >= U) return;
     const unsigned i = V[t];
-    const u64 hi = H[t];
     // Suffixes shorter than h (padded with the smallest code) order by length
     // before every longer member of their group: lo = remaining length in
     // [1, h]; otherwise h + 1 + rank of suffix i + h.
     u64 lo = ((long long)i + h < n) ? (u64)(h + 1) + isa[i + h] : (u64)(n - i);
-    keys[t] = hi * (u64)(n + h + 1) + lo;
+    keys[t] = ((u64)G[t] << lo_bits) | lo;
     vals[t] = i;
+}
+
+// Dense ordinal of each list entry's group (runs of equal heads): exclusive
+// count of run starts, block scan + decoupled look-back; total -> *groups.
+constexpr int kGNT = 256, kGIPT = 8, kGTile = kGNT * kGIPT;
+__global__ void __launch_bounds__(kGNT) k_group_ordinals(const unsigned *__restrict__ H, long long U,
+                                                       unsigned *__restrict__ G, unsigned long long *groups,
+                                                       unsigned *counter, u64 *status, long long tiles) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned s_warp[kGNT / 32];
+    __shared__ u64 s_base;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const long long tile = s_tile;
+    const long long t0 = tile * kGTile + (long long)threadIdx.x * kGIPT;
+    unsigned starts = 0, cnt = 0;
+    unsigned prev = (t0 > 0 && t0 - 1 < U) ? H[t0 - 1] : 0xffffffffu;
+    unsigned hv[kGIPT];
+    const bool full = t0 + kGIPT <= U;
+    if (full) {  // two 16-byte loads
+        const uint4 *q = reinterpret_cast<const uint4 *>(H + t0);
+        const uint4 a = q[0], b = q[1];
+        hv[0] = a.x; hv[1] = a.y; hv[2] = a.z; hv[3] = a.w;
+        hv[4] = b.x; hv[5] = b.y; hv[6] = b.z; hv[7] = b.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kGIPT; ++j) hv[j] = t0 + j < U ? H[t0 + j] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kGIPT; ++j) {
+        const long long t = t0 + j;
+        if (t < U) {
+            const bool f = t == 0 || hv[j] != prev;
+            starts |= (unsigned)f << j;
+            cnt += f;
+            prev = hv[j];
+        }
+    }
+    unsigned excl;
+    const unsigned tot = block_exclusive_sum<kGNT>(cnt, excl, s_warp);
+    if (threadIdx.x < 32) {
+        const u64 base = lookback_warp(status, tile, (u64)tot, OpSum());
+        if (threadIdx.x == 0) {
+            s_base = base;
+            if (tile == tiles - 1) *groups = base + tot;
+        }
+    }
+    __syncthreads();
+    u64 g = s_base + excl;  // run starts before this thread's items
+    unsigned gv[kGIPT];
+#pragma unroll
+    for (int j = 0; j < kGIPT; ++j) {
+        if (starts >> j & 1) ++g;
+        gv[j] = (unsigned)(g - 1);
+    }
+    if (full) {
+        uint4 *q = reinterpret_cast<uint4 *>(G + t0);
+        q[0] = make_uint4(gv[0], gv[1], gv[2], gv[3]);
+        q[1] = make_uint4(gv[4], gv[5], gv[6], gv[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kGIPT; ++j)
+            if (t0 + j < U) G[t0 + j] = gv[j];
+    }
 }
 
 constexpr int kUNT = 256;
@@ -294,6 +360,13 @@ __global__ void __launch_bounds__(kUNT, 4) k_update(const KeyT *__restrict__ key
             V_next[o] = v;
             ++o;
         }
+    }
+    if (sb.group_count) {  // still-tied groups (sizes the next round's keys)
+        unsigned gs = 0;
+#pragma unroll
+        for (int j = 0; j < kUIPT; ++j) gs += (t0 + j < U) && newf[j] && (unsorted >> j & 1);
+        gs = __reduce_add_sync(0xffffffffu, gs);
+        if (lane == 0 && gs) atomicAdd(sb.group_count, (unsigned long long)gs);
     }
     if (P) {
         if (be.stage) {  // large later rounds: ISA through the bucketed scatter too
@@ -1043,7 +1116,7 @@ void build_suffix_array(rs_ctx *c, long long n) {
     long long U = n;
     const unsigned *P = nullptr;
     long long depth = K;
-    const SegBoundary sb_whole{n, 0, 0};
+    SegBoundary sb_whole{n, 0, 0, nullptr};
     c->isa_lazy = false;
     while (true) {
         ++c->sa_rounds;
@@ -1052,6 +1125,8 @@ void build_suffix_array(rs_ctx *c, long long n) {
         u64 *tpre = tagg + tiles + 1;
         BucketEmit be{nullptr, nullptr, 0, 0, nullptr};
         bool skip_isa = false;
+        RS_CUDA(cudaMemsetAsync(u_dev + 1, 0, sizeof(unsigned long long), c->stream));
+        sb_whole.group_count = u_dev + 1;
         if (P && U >= n / 16) be = bucket_setup(c, n, 0, false);
         // Round 0: the tied count is known after the reduce pass.  With few
         // ties (i.i.d.-like text) the SA after round 0 + the small-group sort
@@ -1095,8 +1170,13 @@ void build_suffix_array(rs_ctx *c, long long n) {
             if (idv == B_VALS0) v0 = (unsigned *)c->bufs[B_VALS0].p;
             else v1 = (unsigned *)c->bufs[B_VALS1].p;
         }
-        unsigned long long un = 0;
-        fetch_small(c, &un, u_dev, sizeof(un));
+        unsigned long long un = 0, ngroups = 0;
+        {
+            unsigned long long two[2];
+            fetch_small(c, two, u_dev, sizeof(two));
+            un = two[0];
+            ngroups = two[1];
+        }
         add_bytes_last(c, 4.0 * (double)un);
         // skip_isa (few ties): raw is applied after k_small_groups added the tied suffixes
         if (!P) {
@@ -1148,10 +1228,25 @@ void build_suffix_array(rs_ctx *c, long long n) {
         std::swap(Ha, Hb);
         std::swap(Va, Vb);
         P = Pb;
-        RS_LAUNCH_B(c, 20.0 * U, k_make_keys, grid_for(U, 256), 256, 0, Hb, Vb, U, isa, n, depth, k0, v0);
-        // bits of a round key hi*(n+h+1)+lo < n*(n+h+1)
-        int rbits = (int)std::ceil(std::log2((double)n * (double)(n + depth + 1)));
-        if (rbits < 1) rbits = 1;
+        // round key (group, lo): the group as its head slot, or -- when it
+        // saves radix passes (few large groups, e.g. periodic text) -- as the
+        // group's dense ordinal (Pa is free here: the lists live in Pb/Hb/Vb)
+        int lo_bits = 1;
+        while ((1ull << lo_bits) <= (unsigned long long)(n + depth + 1)) ++lo_bits;
+        int g_bits = 0;
+        while ((1ull << g_bits) < ngroups) ++g_bits;
+        int h_bits = 0;
+        while ((1ull << h_bits) < (unsigned long long)n) ++h_bits;
+        const bool dense = (lo_bits + g_bits + 7) / 8 < (lo_bits + h_bits + 7) / 8;
+        if (dense) {
+            const long long gt = (U + kGTile - 1) / kGTile;
+            Scratch sc = scratch(c, gt);
+            RS_LAUNCH_B(c, 8.0 * U, k_group_ordinals, (unsigned)gt, kGNT, 0, Hb, U, Pa, u_dev, sc.counter, sc.status,
+                        gt);
+        }
+        RS_LAUNCH_B(c, 20.0 * U, k_make_keys, grid_for(U, 256), 256, 0, dense ? Pa : Hb, Vb, U, isa, n, depth,
+                    lo_bits, k0, v0);
+        const int rbits = std::max(1, lo_bits + (dense ? g_bits : h_bits));
         radix_sort_pairs<u64>(c, k0, k1, v0, v1, U, rbits, &ks, &vs);
         depth *= 2;
     }
@@ -1334,7 +1429,7 @@ void dist_update(rs_ctx *c, long long n, int rank, int world, const long long *n
     const u64 *stream = (const u64 *)c->bufs[B_PACKED].p;
     BucketEmit be = bucket_setup(c, n, 0, false);
     if (m > 0) {
-        SegBoundary sb{n, 0u, 0u};
+        SegBoundary sb{n, 0u, 0u, nullptr};
         if (nbr[2])
             sb.lcp_first = host_key_lcp(c->dist.first_key, (unsigned long long)nbr[0], bits, key_bits, (unsigned)K,
                                         (unsigned)(n - c->dist.first_pos), (unsigned)(n - nbr[1]));
