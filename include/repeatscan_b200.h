@@ -186,7 +186,8 @@ int rs_summarize_steps(rs_ctx *ctx, const int64_t *steps, int64_t count, int64_t
 #define RS_BUF_TEXT 4  /* uint8 text (n + 128 bytes; rs_set_text_device) */
 #define RS_BUF_SEND 5  /* distributed sort: (position, raw) uint32 pairs bound for other ranks */
 #define RS_BUF_RAW 6   /* distributed sort: this rank's raw LLR shard incl. its left halo */
-/* Ensure >= bytes of device buffer `which` and return its device pointer. */
+/* Ensure >= bytes of device buffer `which` and return its device pointer; a request
+ * within the current capacity never reallocates (contents stay valid). */
 int rs_device_buffer(rs_ctx *ctx, int which, int64_t bytes, void **ptr);
 /* Declare that RS_BUF_LLRC holds m valid entries of a text of length n
  * (validated on device like rs_set_compact). */

@@ -864,7 +864,9 @@ int rs_device_buffer(rs_ctx *c, int which, int64_t bytes, void **ptr) {
     return guarded(c, [&] {
         static const BufId ids[7] = {B_LLRC, B_OUT0, B_OUT1, B_FLAT, B_TEXT, B_SEND, B_RAW};
         if (which < 0 || which > 6 || bytes < 0 || !ptr) fail(RS_EINVAL, "bad buffer request");
-        *ptr = buf(c, ids[which], (size_t)bytes + 64 + (which == RS_BUF_TEXT ? 128 : 0));
+        // exactly `bytes` (+ the text's zero pad): a request within the current
+        // capacity never reallocates, so views of filled buffers stay valid
+        *ptr = buf(c, ids[which], (size_t)bytes + (which == RS_BUF_TEXT ? 128 : 0));
     });
 }
 
