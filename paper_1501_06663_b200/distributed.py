@@ -4,8 +4,9 @@ Positions are independent reads of immutable candidate arrays with disjoint
 output slots (engine.py:3-7), so the path shards by POSITION:
 
 1. rank 0 builds the suffix structures, raw LLR and the compact array LLRc of
-   the whole text on its GPU (the suffix sort is not sharded yet: SURVEY
-   8(f)#1 is the next row);
+   the whole text on its GPU (the replicated-structures path,
+   `sharded_all_positions`; `dist_sa_all_positions` further down shards the
+   suffix sort itself -- SURVEY 8(f)#1 -- for texts without long repeats);
 2. LLRc (8 bytes per entry) is broadcast with NCCL over NVLink, straight
    from/into the library's device buffers (zero-copy torch views);
 3. rank r answers the contiguous position shard [lo_r, hi_r) of
@@ -471,16 +472,18 @@ def loopback_dist_all_positions(data: np.ndarray, world: int, mode: str = "all",
             applies.append(dist_phase_apply(c, q, world, recv.data_ptr(), recv.numel()))
             del recv
         halo = max(int(a[3]) for a in applies) + 2
-        if halo + 4 > HALO_CAP:
+        if not dist_halo_fits(n, world, halo):
             return None
-        for r in range(world - 1):
+        partners = dist_halo_partners(n, world)
+        for r in range(world):
             P0, P1 = int(applies[r][1]), int(applies[r][2])
-            if P1 <= P0 or int(applies[r + 1][2]) <= int(applies[r + 1][1]):
+            q = partners[r][1]
+            if P1 <= P0 or q < 0:
                 continue
             lo = max(P1 + 1 - halo, 1)
             cnt = P1 + 1 - lo
             src = _raw_view(ctxs[r], applies[r], lo, cnt, device)
-            dst = _raw_view(ctxs[r + 1], applies[r + 1], lo, cnt, device)
+            dst = _raw_view(ctxs[q], applies[q], lo, cnt, device)
             dst.copy_(src)
         torch.cuda.synchronize(device)
         totals = [dist_phase_scan(c, mode, halo) for c in ctxs]
@@ -517,6 +520,26 @@ def _assemble_host(ctxs, applies, totals, n: int, mode: str):
         offsets[P0 + 1:P1 + 2] = offs
         base += t
     return lengths, offsets, flat
+
+
+def dist_halo_partners(n: int, world: int) -> list[tuple[int, int]]:
+    """Per rank (previous, next) rank with a non-empty position shard (-1 if
+    none); only ranks with non-empty shards exchange halos (with few buckets,
+    empty shards can sit between non-empty ones)."""
+    nonempty = [r for r in range(world) if dist_shard(n, r, world)[1] > dist_shard(n, r, world)[0]]
+    out = []
+    for r in range(world):
+        prev = max((q for q in nonempty if q < r), default=-1)
+        nxt = min((q for q in nonempty if q > r), default=-1)
+        out.append((prev, nxt))
+    return out
+
+
+def dist_halo_fits(n: int, world: int, halo: int) -> bool:
+    """The left halo of every shard must come from ONE neighbour: `halo` may not
+    exceed any non-empty shard that has a later non-empty shard."""
+    sizes = [b - a for a, b in (dist_shard(n, r, world) for r in range(world)) if b > a]
+    return halo + 4 <= HALO_CAP and all(halo <= s for s in sizes[:-1])
 
 
 def dist_shard(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -585,21 +608,21 @@ def dist_sa_all_positions(data: np.ndarray | None, n: int, mode: str = "all", gr
         mx = torch.tensor([int(ainfo[3])], **kw)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
         halo = int(mx.item()) + 2
-        if halo + 4 > HALO_CAP:
+        if not dist_halo_fits(n, world, halo):
             return None
         # left halo: the last `halo` raw values of the previous non-empty shard
         P0, P1 = int(ainfo[1]), int(ainfo[2])
         ops = []
-        if P1 > P0 and rank + 1 < world:
-            q0, q1 = dist_shard(n, rank + 1, world)
-            if q1 > q0:
-                lo = max(P1 + 1 - halo, 1)
+        prev_r, next_r = dist_halo_partners(n, world)[rank]
+        if P1 > P0 and next_r >= 0:
+            lo = max(P1 + 1 - halo, 1)
+            if P1 + 1 - lo > 0:
                 ops.append(dist.P2POp(dist.isend, _raw_view(ctx, ainfo, lo, P1 + 1 - lo, device).contiguous(),
-                                      rank + 1, group))
-        if P1 > P0 and rank > 0:
+                                      next_r, group))
+        if P1 > P0 and prev_r >= 0:
             lo = max(P0 + 1 - halo, 1)
-            buf_in = _raw_view(ctx, ainfo, lo, P0 + 1 - lo, device)
-            ops.append(dist.P2POp(dist.irecv, buf_in, rank - 1, group))
+            if P0 + 1 - lo > 0:
+                ops.append(dist.P2POp(dist.irecv, _raw_view(ctx, ainfo, lo, P0 + 1 - lo, device), prev_r, group))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()

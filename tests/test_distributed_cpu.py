@@ -116,3 +116,14 @@ def test_dist_neighbours():
     assert nb[0] == [0, 0, 0, 20, 200, 1]           # next non-empty segment is rank 2
     assert nb[2] == [11, 101, 1, 30, 300, 1]        # previous non-empty is rank 0
     assert nb[3] == [21, 201, 1, 0, 0, 0]
+
+
+def test_dist_halo_partners_skip_empty_shards():
+    from paper_1501_06663_b200.distributed import dist_halo_fits, dist_halo_partners, dist_shard
+    # 3 buckets over 5 ranks: shards 0 and 2 are empty
+    shards = [dist_shard(10_000, r, 5) for r in range(5)]
+    assert [b - a for a, b in shards] == [0, 4096, 0, 4096, 1808]
+    assert dist_halo_partners(10_000, 5) == [(-1, 1), (-1, 3), (1, 3), (1, 4), (3, -1)]
+    assert dist_halo_fits(10_000, 5, 4096) and not dist_halo_fits(10_000, 5, 4097)
+    # the last non-empty shard never sends a halo, its size does not bound it
+    assert dist_halo_fits(10_000, 3, 4000)

@@ -391,6 +391,19 @@ def test_distributed_suffix_sort_loopback():
         assert np.array_equal(got[0], ws) and np.array_equal(got[1], wln), ci
 
 
+def test_distributed_suffix_sort_more_ranks_than_buckets():
+    # n = 10000 -> 3 position buckets: with 5 or 7 ranks some position shards
+    # (and SA segments) are empty, between non-empty ones; the halo comes from
+    # the nearest non-empty shard
+    from paper_1501_06663_b200 import distributed as D
+    data = workloads.iid_dna(10_000, 31)
+    wl, wo, wf = oracle.all_positions(data, mode="all")
+    for world in (4, 5, 7):
+        got = D.loopback_dist_all_positions(data, world, "all")
+        assert got is not None, world
+        assert np.array_equal(got[0], wl) and np.array_equal(got[1], wo) and np.array_equal(got[2], wf), world
+
+
 def test_distributed_suffix_sort_declines_repetitive_text():
     from paper_1501_06663_b200 import distributed as D
     data = workloads.periodic_mutated(50_000, 3, period=7, rate=0.0)
