@@ -1553,8 +1553,10 @@ void dist_scan(rs_ctx *c, long long n, int mode, long long halo, long long *tota
     c->shard_hi = P1 + 1;
     if (cnt > 0) {
         const unsigned *d_raw = (const unsigned *)c->bufs[B_RAW].p - c->dist.R0;
+        // long repeats (a window beyond the fused kernel's shared stage): the
+        // raw-path scan over the same shard + halo (same answers, Lemma 2)
         if (!query_range(c, mode, RS_PATH_COMPACT, nullptr, 0, d_raw, P0 + 1, P1, 0, cnt, P0 + 1 - halo))
-            fail(RS_ERANGE, "repeats too long for the distributed scan");
+            query_range(c, mode, RS_PATH_RAW, nullptr, 0, d_raw, P0 + 1, P1, 0, cnt, P0 + 1 - halo);
     }
     *total = mode == RS_MODE_ALL ? c->total : 0;
 }

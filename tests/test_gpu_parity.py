@@ -160,6 +160,35 @@ def test_random_inputs_vs_oracle(rng):
         assert np.array_equal(A.flat_starts, wf)
 
 
+def test_medium_random_texts_vs_oracle(rng):
+    # sizes where the multi-round paths engage (u64 keys, dense-ordinal
+    # keys, small-group resolution, lazy ISA, Kasai vs patch LCP), mixed
+    # alphabets, planted copies and periodic stretches
+    for case in range(10):
+        n = int(rng.integers(100_000, 1_500_000))
+        sigma = int(rng.choice([2, 3, 4, 5, 20, 95, 256]))
+        alpha = rng.choice(256, size=sigma, replace=False).astype(np.uint8)
+        data = rng.choice(alpha, size=n)
+        for _ in range(int(rng.integers(0, 6))):  # planted copies
+            ln = int(rng.integers(10, 5000))
+            src, dst = (int(x) for x in rng.integers(0, n - ln, 2))
+            data[dst:dst + ln] = data[src:src + ln].copy()
+        if case % 3 == 0:  # a periodic stretch
+            p, ln = int(rng.integers(1, 40)), int(rng.integers(1000, 50_000))
+            dst = int(rng.integers(0, n - ln))
+            data[dst:dst + ln] = np.resize(data[:p], ln)
+        want = oracle.build_suffix_structures(data)
+        s = rb.build_suffix_structures(rb.Text(data))
+        assert all(np.array_equal(a, b) for a, b in zip((s.sa, s.rank, s.lcp), want)), (case, n, sigma)
+        wl, wo, wf = oracle.all_positions(data, mode="all", structures=want)
+        A = rb.all_positions(rb.Text(data), mode="all")
+        assert np.array_equal(A.lengths, wl) and np.array_equal(A.offsets, wo), (case, n, sigma)
+        assert np.array_equal(A.flat_starts, wf), (case, n, sigma)
+        ws, wln = oracle.all_positions(data, mode="leftmost", structures=want)
+        L = rb.all_positions(rb.Text(data), mode="leftmost", path="compact")
+        assert np.array_equal(L.starts, ws) and np.array_equal(L.lengths, wln), (case, n, sigma)
+
+
 def test_tile_boundaries_and_long_windows():
     # sizes straddling the 2048-position tiles and 4096-key sort tiles,
     # plus a periodic text whose windows exceed the shared-memory stage.
