@@ -99,9 +99,9 @@ __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict
 // candidate fills the positions where it is the boundary -- O(tile +
 // candidates), no searches -- unless candidates are few and long
 // (repetitive text), then one binary search per position.
-template <bool RAW>
+template <bool RAW, typename IdxT>
 __device__ __forceinline__ void fill_windows(const Cand<RAW> &c, unsigned cnt, int tile_k0, int tile_k1, int npos,
-                                             unsigned *s_lo, unsigned *s_hi) {
+                                             IdxT *s_lo, IdxT *s_hi) {
     if (cnt * 8 < (unsigned)npos) {
         for (int p = threadIdx.x; p < npos; p += kNT) {
             const int k = tile_k0 + p;
@@ -110,13 +110,13 @@ __device__ __forceinline__ void fill_windows(const Cand<RAW> &c, unsigned cnt, i
                 const unsigned mid = (a + b) >> 1;
                 if (c.end(mid) >= k) b = mid; else a = mid + 1;
             }
-            s_lo[p] = a;
+            s_lo[p] = (IdxT)a;
             b = cnt;
             while (a < b) {
                 const unsigned mid = (a + b) >> 1;
                 if ((int)c.start(mid) <= k) a = mid + 1; else b = mid;
             }
-            s_hi[p] = a;
+            s_hi[p] = (IdxT)a;
         }
     } else {
         for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
@@ -125,22 +125,26 @@ __device__ __forceinline__ void fill_windows(const Cand<RAW> &c, unsigned cnt, i
             int a = ep + 1 > tile_k0 ? ep + 1 : tile_k0;
             int b = e_t < tile_k1 ? e_t : tile_k1;
 #pragma unroll 1
-            for (int k = a; k <= b; ++k) s_lo[k - tile_k0] = t;
+            for (int k = a; k <= b; ++k) s_lo[k - tile_k0] = (IdxT)t;
             const int st = (int)c.start(t);
             const int sn = (t + 1 < cnt) ? (int)c.start(t + 1) : tile_k1 + 1;
             a = st > tile_k0 ? st : tile_k0;
             b = sn - 1 < tile_k1 ? sn - 1 : tile_k1;
 #pragma unroll 1
-            for (int k = a; k <= b; ++k) s_hi[k - tile_k0] = t + 1;
+            for (int k = a; k <= b; ++k) s_hi[k - tile_k0] = (IdxT)(t + 1);
         }
     }
     __syncthreads();
 }
 
+// IdxT: per-position window bounds (u16 in the fused kernel, whose windows
+// index a shared stage of < 2^16 entries: smaller footprint, 8 CTAs per SM)
+template <typename IdxT>
 struct TileCtx {
     long long tile, cnt, tile_k0, tile_k1, slot0, tiles, flat_cap;
     int npos, out_off;
-    unsigned *s_lo, *s_hi, *s_cnt, *s_warp;
+    IdxT *s_lo, *s_hi;
+    unsigned *s_cnt, *s_warp;
     u64 *s_base;
     long long *out0, *out1, *flat;
     u64 *status;
@@ -150,10 +154,10 @@ struct TileCtx {
 // Everything after staging.  Inlined twice (candidates in shared memory or,
 // for oversized windows, in global memory) so each copy uses the right
 // address space (LDS instead of generic loads).
-template <bool RAW, bool ALL>
-__device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx &x) {
+template <bool RAW, bool ALL, typename IdxT>
+__device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<IdxT> &x) {
     const unsigned cnt = (unsigned)x.cnt;
-    fill_windows<RAW>(c, cnt, (int)x.tile_k0, (int)x.tile_k1, x.npos, x.s_lo, x.s_hi);
+    fill_windows<RAW, IdxT>(c, cnt, (int)x.tile_k0, (int)x.tile_k1, x.npos, x.s_lo, x.s_hi);
 
     // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
     // Windows of up to 32 candidates (the common case) record their ties as a
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     } else {
         tile = blockIdx.x;
     }
-    TileCtx x;
+    TileCtx<unsigned> x;
     x.tile = tile;
     const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];
     x.cnt = hi - lo;
@@ -389,7 +393,11 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
 // path when every tile's raw range fits the stage (short repeats).
 constexpr int kFStage = kG + 1024 + 16;  // staged raw values incl. alignment slack and slot lo-1
 constexpr int kFRawBytes = ((4 * kFStage + 127) / 128) * 128;
-constexpr int kFusedSmem = kFRawBytes + 8 * kFStage + 3 * 4 * kG;
+// the raw stage is dead after compaction: the per-position window bounds
+// (u16) and tie counts reuse it -> ~25 KB per CTA, 8 CTAs per SM
+static_assert(2 * 2 * kG + 4 * kG <= kFRawBytes, "window bounds + counts must fit the raw stage");
+static_assert(kFStage < 65536, "u16 window bounds");
+constexpr int kFusedSmem = kFRawBytes + 8 * kFStage;
 
 template <bool ALL>
 __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict__ raw, long long kb, long long ke,
@@ -414,7 +422,7 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
     } else {
         tile = blockIdx.x;
     }
-    TileCtx x;
+    TileCtx<unsigned short> x;
     x.tile = tile;
     const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];  // raw slots [lo, hi)
     x.tile_k0 = kb + tile * kG;
@@ -424,9 +432,9 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
     x.out_off = out_off;
     x.tiles = tiles;
     x.flat_cap = flat_cap;
-    x.s_lo = reinterpret_cast<unsigned *>(dsm + kFRawBytes + 8 * kFStage);
+    x.s_lo = reinterpret_cast<unsigned short *>(dsm);  // aliases s_raw (dead after compaction)
     x.s_hi = x.s_lo + kG;
-    x.s_cnt = x.s_hi + kG;
+    x.s_cnt = reinterpret_cast<unsigned *>(dsm + 4 * kG);
     x.s_warp = s_warp;
     x.s_base = &s_base;
     x.out0 = out0;
@@ -461,8 +469,9 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
         if (o < nr && r0[o] > 0u && r0[o] >= r0[o - 1]) s_list[w++] = make_uint2((unsigned)(lo + o), r0[o]);
     }
     x.cnt = cnt;
+    __syncthreads();  // s_raw dead from here: the window bounds take its place
     for (int i = threadIdx.x; i < x.npos; i += kNT) {
-        x.s_lo[i] = cnt;
+        x.s_lo[i] = (unsigned short)cnt;
         x.s_hi[i] = 0;
     }
     __syncthreads();
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(kNT) k_steps(const uint2 *__restrict__ e, cons
         c.e = RAW ? nullptr : e + lo;
         c.r = RAW ? raw + lo : nullptr;
     }
-    fill_windows<RAW>(c, (unsigned)(cnt > 0 ? cnt : 0), (int)tile_k0, (int)(tile_k0 + npos - 1), npos, s_lo, s_hi);
+    fill_windows<RAW, unsigned>(c, (unsigned)(cnt > 0 ? cnt : 0), (int)tile_k0, (int)(tile_k0 + npos - 1), npos, s_lo, s_hi);
     unsigned long long mn = ~0ull, mx = 0, sum = 0, n = 0;
     for (int p = threadIdx.x; p < npos; p += kNT) {
         const long long w = (long long)s_hi[p] - (long long)s_lo[p];
