@@ -208,7 +208,8 @@ int rs_fetch_shard(rs_ctx *ctx, int mode, int64_t *a, int64_t *b, int64_t *flat)
  * balanced on the digit histogram), i.e. one contiguous segment of the SA.
  * Raw LLR leaves in text order through an all-to-all of (position, raw)
  * pairs into bucket-aligned position shards, each rank then scans its shard
- * (left halo of `halo` raw values received from the previous rank).
+ * (left halo of `halo` raw values received from the nearest earlier rank
+ * with a non-empty shard; `halo` may not exceed that shard's length).
  * Supported regime: 32-bit symbol-aligned round-0 keys and tied groups of at
  * most 8 suffixes (i.i.d.-like text); info[0] = 0 otherwise and the caller
  * runs the single-GPU path.
@@ -222,9 +223,10 @@ int rs_fetch_shard(rs_ctx *ctx, int mode, int64_t *a, int64_t *b, int64_t *flat)
  *                  halo_cap = halo slots reserved before the shard;
  *                  info = [ok, P0, P1 (0-based shard), max raw, R0]; the
  *                  shard's raw array (RS_BUF_RAW) holds raw[i] at [i - R0]
- *   rs_dist_scan   all-ties / leftmost scan of the shard, outputs as
- *                  rs_query_shard (rebase / fetch with rs_shard_rebase,
- *                  rs_fetch_shard). */
+ *   rs_dist_scan   all-ties / leftmost scan of the shard (fused compact
+ *                  scan; raw-path scan when a window exceeds its shared
+ *                  stage), outputs as rs_query_shard (rebase / fetch with
+ *                  rs_shard_rebase, rs_fetch_shard). */
 int rs_set_text_device(rs_ctx *ctx, int64_t n);
 int rs_dist_sort(rs_ctx *ctx, int32_t rank, int32_t world, int64_t *info);
 int rs_dist_update(rs_ctx *ctx, int32_t rank, int32_t world, const int64_t *nbr, int64_t *send_counts,
