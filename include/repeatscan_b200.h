@@ -211,8 +211,9 @@ int rs_fetch_shard(rs_ctx *ctx, int mode, int64_t *a, int64_t *b, int64_t *flat)
  * (left halo of `halo` raw values received from the nearest earlier rank
  * with a non-empty shard; `halo` may not exceed that shard's length).
  * Supported regime: 32-bit symbol-aligned round-0 keys and tied groups of at
- * most 8 suffixes (i.i.d.-like text); info[0] = 0 otherwise and the caller
- * runs the single-GPU path.
+ * most 1025 suffixes whose common prefixes stay below 4096 symbols (i.i.d. or
+ * planted-repeat DNA); info[0] = 0 otherwise and the caller runs the
+ * single-GPU path.
  *   rs_dist_sort   info[16]: [ok, m, S (first SA slot), first key, first
  *                  suffix, last key, last suffix, bits, K]
  *   rs_dist_update nbr[6] = prev rank's (last key, last suffix, has_prev),

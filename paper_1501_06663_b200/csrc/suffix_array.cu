@@ -738,15 +738,7 @@ __global__ void __launch_bounds__(kSGNT) k_small_groups_seg(const unsigned *__re
         while (back < kSmallGroup && t - back - 1 >= 0 && H[t - back - 1] == head) ++back;
         while (fwd < kSmallGroup && t + fwd + 1 < U && H[t + fwd + 1] == head) ++fwd;
         const bool small = back + fwd + 1 <= kSmallGroup;
-        keep[t] = small ? 0u : 1u;
-        if (!small) {  // left to the doubling rounds: round-0 raw candidate (unknown LCPs as 0)
-            const unsigned slot = P[t];
-            unsigned a = lcp_d[slot], c2 = lcp_d[slot + 1];
-            a = a == kLcpUnknown ? 0u : a;
-            c2 = c2 == kLcpUnknown ? 0u : c2;
-            s_dest[threadIdx.x] = V[t];
-            s_val[threadIdx.x] = a > c2 ? a : c2;
-        }
+        keep[t] = small ? 0u : 1u;  // larger groups: k_large_groups_seg sorts and emits them
         const bool starter = small && back == 0;
         if (starter || (small && back > 0 && t == tb)) {
             const long long g0 = t - back;  // first entry of the group
@@ -1074,6 +1066,165 @@ TextPrep prepare_text(rs_ctx *c, long long n) {
     return TextPrep{stream, words, bits, K, sigma};
 }
 
+// ---- distributed path: tied groups larger than kSmallGroup -----------------
+// suffix_less with a depth cap: `over` is set when the common prefix reaches
+// `cap` symbols (the caller then declines the whole text).
+__device__ __forceinline__ bool suffix_less_capped(const u64 *__restrict__ stream, int b, long long n, long long K,
+                                                   unsigned a, unsigned c, long long cap, bool &over) {
+    const long long lim = n - (long long)(a > c ? a : c);
+    long long h = K < lim ? K : lim;
+    const int per = 64 / b;
+    while (h < lim) {
+        if (h >= cap) {
+            over = true;
+            return a < c;
+        }
+        const u64 wa = load_sym64(stream, b, (long long)a + h), wc = load_sym64(stream, b, (long long)c + h);
+        const u64 x = wa ^ wc;
+        if (x == 0) {
+            h += per;
+            continue;
+        }
+        h += __clzll((long long)x) / b;
+        if (h >= lim) break;
+        return wa < wc;
+    }
+    return a > c;  // one is a prefix of the other: the shorter (later start) sorts first
+}
+
+constexpr int kLGB = 1024;         // list entries per block (rounded out to whole groups)
+constexpr int kLGSlots = 2 * kLGB; // sort capacity: groups of up to kLGB + 1 members always fit
+constexpr int kLGCap = 4096;       // longest common prefix (symbols) inside a group
+constexpr int kLGNT = 256;
+
+// First group boundary (head change; U counts as one) at or after x.
+__device__ __forceinline__ long long next_group_start(const unsigned *__restrict__ H, long long U, long long x,
+                                                      int *s_min) {
+    long long base = x;
+    while (true) {
+        if (threadIdx.x == 0) *s_min = 0x7fffffff;
+        __syncthreads();
+        const long long t = base + threadIdx.x;
+        const bool f = t >= U || t == 0 || H[t] != H[t - 1];
+        if (f) atomicMin(s_min, (int)threadIdx.x);
+        __syncthreads();
+        const int m = *s_min;
+        __syncthreads();
+        if (m != 0x7fffffff) return base + m;
+        base += kLGNT;
+    }
+}
+
+// Tied groups above kSmallGroup members after round 0 (runs of equal heads in
+// the (slot, head, suffix) lists).  Block b takes the whole groups that start
+// in list entries [b kLGB, (b + 1) kLGB) and bitonic-sorts them together by
+// (head, suffix) -- members compared by their cached first window past the
+// shared key, else by packed-text comparison -- then writes SA slots, the LCPs
+// of adjacent members and their raw LLR values (group boundary LCPs are known
+// from round 0) into the bucketed scatter.  A group of more than kLGB + 1
+// members or with a common prefix of kLGCap symbols sets *decline.
+__global__ void __launch_bounds__(kLGNT) k_large_groups_seg(const unsigned *__restrict__ P,
+                                                        const unsigned *__restrict__ H,
+                                                        const unsigned *__restrict__ V, long long U,
+                                                        const u64 *__restrict__ stream, int b, long long n,
+                                                        long long K, unsigned *__restrict__ sa,
+                                                        unsigned *__restrict__ lcp_d, BucketEmit be,
+                                                        unsigned *decline) {
+    __shared__ EmitSmem<kLGNT, 1> s_emit;
+    __shared__ unsigned s_v[kLGSlots], s_h[kLGSlots];
+    __shared__ u64 s_w[kLGSlots];  // first window past the shared round-0 key
+    __shared__ unsigned s_l[kLGSlots + 1];
+    __shared__ int s_min, s_over;
+    const long long lo = (long long)blockIdx.x * kLGB;
+    const long long hi = lo + kLGB < U ? lo + kLGB : U;
+    const long long s0 = next_group_start(H, U, lo, &s_min);
+    if (s0 >= hi) return;  // every entry here belongs to a group started earlier
+    const long long s1 = next_group_start(H, U, hi, &s_min);
+    const int m = (int)(s1 - s0);
+    if (m > kLGSlots) {
+        if (threadIdx.x == 0) atomicOr(decline, 1u);
+        return;
+    }
+    int p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += kLGNT) {
+        const bool real = i < m;
+        const unsigned v = real ? V[s0 + i] : 0xffffffffu;
+        s_v[i] = v;
+        s_h[i] = real ? H[s0 + i] : 0xffffffffu;
+        s_w[i] = real ? load_sym64(stream, b, (long long)v + K) : 0;
+    }
+    if (threadIdx.x == 0) s_over = 0;
+    __syncthreads();
+    bool over = false;
+    for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < p2; i += kLGNT) {
+                const int q = i ^ j;
+                if (q <= i) continue;
+                const unsigned x = s_v[i], y = s_v[q], hx = s_h[i], hy = s_h[q];
+                const u64 wx = s_w[i], wy = s_w[q];
+                // (head, suffix) order; padding (head 0xffffffff) sorts last
+                bool lt;
+                if (hx != hy) {
+                    lt = hx < hy;
+                } else if (hx == 0xffffffffu) {
+                    lt = false;
+                } else {
+                    const long long lim = n - (long long)(x > y ? x : y);
+                    const u64 d = wx ^ wy;
+                    if (d != 0 && K + __clzll((long long)d) / b < lim) lt = wx < wy;
+                    else lt = suffix_less_capped(stream, b, n, K, x, y, kLGCap, over);
+                }
+                const bool up = (i & k) == 0;  // ascending half of the bitonic merge
+                if (up ? !lt : lt) {
+                    s_v[i] = y;
+                    s_v[q] = x;
+                    s_h[i] = hy;
+                    s_h[q] = hx;
+                    s_w[i] = wy;
+                    s_w[q] = wx;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (over) s_over = 1;
+    __syncthreads();
+    if (s_over) {
+        if (threadIdx.x == 0) atomicOr(decline, 1u);
+        return;
+    }
+    // s_l[i] = LCP of sorted members i-1, i; at a group's first member (and
+    // past the last) the boundary LCP with the neighbouring slot, from round 0
+    for (int i = threadIdx.x; i <= m; i += kLGNT) {
+        unsigned l;
+        if (i == m) {
+            l = lcp_d[P[s1 - 1] + 1];
+        } else if (i == 0 || s_h[i] != s_h[i - 1]) {
+            l = lcp_d[P[s0 + i]];
+        } else {
+            const long long a = s_v[i - 1], c = s_v[i];
+            const long long lim = n - (a > c ? a : c);
+            l = (unsigned)packed_lcp(stream, b, a, c, K < lim ? K : lim, lim);
+        }
+        s_l[i] = l;
+    }
+    __syncthreads();
+    for (int i0 = 0; i0 < m; i0 += kLGNT) {  // uniform trip count: bucket_emit is block-collective
+        const int i = i0 + threadIdx.x;
+        unsigned d = kNoDest, vl = 0;
+        if (i < m) {
+            d = s_v[i];
+            const unsigned slot = P[s0 + i];  // groups keep their slot ranges: list order is slot order
+            sa[slot] = d;
+            if (i > 0 && s_h[i] == s_h[i - 1]) lcp_d[slot] = s_l[i];
+            vl = s_l[i] > s_l[i + 1] ? s_l[i] : s_l[i + 1];
+        }
+        bucket_emit<kLGNT, 1>(be, &d, &vl, s_emit);
+    }
+}
+
 void ensure_isa(rs_ctx *c);
 
 void build_suffix_array(rs_ctx *c, long long n) {
@@ -1322,9 +1473,10 @@ void build_lcp(rs_ctx *c, long long n) {
 // range (ranges balanced on the digit histogram every rank computes from its
 // copy of the text), i.e. one contiguous segment [S, S + m) of the suffix
 // array; the text-order outputs (raw LLR, then the query) are split into
-// bucket-aligned position shards.  Only the i.i.d.-like regime is
-// distributed: 32-bit symbol-aligned round-0 keys and tied groups of at most
-// kSmallGroup suffixes; otherwise the caller runs the single-GPU path.
+// bucket-aligned position shards.  Distributed regime: 32-bit symbol-aligned
+// round-0 keys and tied groups that k_small_groups_seg / k_large_groups_seg
+// sort by direct comparison (<= kLGB + 1 members, common prefix < kLGCap);
+// otherwise the caller runs the single-GPU path.
 
 static unsigned host_key_lcp(unsigned long long a, unsigned long long b, int code_bits, int key_bits, unsigned K,
                              unsigned rem_a, unsigned rem_b) {
@@ -1475,7 +1627,19 @@ void dist_update(rs_ctx *c, long long n, int rank, int world, const long long *n
                         Pb, Hb, Vb, u_dev, ks_.counter, ks_.status, ktiles);
             fetch_small(c, &big, u_dev, sizeof(big));
             info[3] = (long long)big;
-            if (big > 0) return;  // groups that need doubling rounds: not distributed (info[0] = 0)
+            if (big > 0) {  // groups above kSmallGroup: sorted per block of whole groups on this rank
+                unsigned *decline = (unsigned *)((unsigned long long *)buf(c, B_SMALL, 4096) + 9);
+                RS_CUDA(cudaMemsetAsync(decline, 0, sizeof(unsigned), c->stream));
+                const long long blocks = ((long long)big + kLGB - 1) / kLGB;
+                RS_LAUNCH_B(c, 28.0 * big, k_large_groups_seg, (unsigned)blocks, kLGNT, 0, Pb, Hb, Vb,
+                            (long long)big, stream, bits, n, (long long)K, sa, lcp_d, be, decline);
+                unsigned dec = 0;
+                fetch_small(c, &dec, decline, sizeof(dec));
+                if (std::getenv("RS_DEBUG_ROUNDS"))
+                    std::fprintf(stderr, "dist rank %d: %llu suffixes in tied groups above %d%s\n", rank, big,
+                                 kSmallGroup, dec ? " (declined)" : "");
+                if (dec) return;  // a group too large or too repetitive: not distributed (info[0] = 0)
+            }
         }
     }
     // per destination rank: the buckets of its position shard, in order

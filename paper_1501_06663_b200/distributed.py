@@ -253,7 +253,7 @@ def to_answers(out, mode: str):
 def bench_main(args) -> None:
     """torchrun bench (N > 1), strong scaling over one text.
 
-    value: device-resident step.  Preferred path (i.i.d.-like
+    value: device-resident step.  Preferred path (DNA-like
     text): every rank holds the text and sorts one segment of the suffix
     array, raw LLR is exchanged all-to-all into position shards and every
     rank scans its shard, keeping its CSR shard in its own HBM.  Texts

@@ -420,6 +420,35 @@ def test_distributed_suffix_sort_loopback():
         assert np.array_equal(got[0], ws) and np.array_equal(got[1], wln), ci
 
 
+def test_distributed_suffix_sort_large_groups():
+    # tied round-0 groups above 8 suffixes (planted repeat families) are sorted
+    # per group on their rank (k_large_groups_seg); > 2048 members declines
+    from paper_1501_06663_b200 import distributed as D
+    rng = np.random.default_rng(41)
+    data = workloads.iid_dna(400_000, 41).copy()
+    for fam, copies in ((0, 40), (1, 300), (2, 12)):
+        src = rng.integers(0, 4, 250).astype(np.uint8)
+        src = np.frombuffer(b"ACGT", np.uint8)[src]
+        for _ in range(copies):
+            dst = int(rng.integers(0, data.size - 250))
+            seg = src.copy()
+            mut = rng.random(250) < 0.03  # diverged copies: many distinct LCPs
+            seg[mut] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, int(mut.sum()))]
+            data[dst:dst + 250] = seg
+    wl, wo, wf = oracle.all_positions(data, mode="all")
+    ws, wln = oracle.all_positions(data, mode="leftmost")
+    for world in (1, 2, 3):
+        got = D.loopback_dist_all_positions(data, world, "all")
+        assert got is not None, world
+        assert np.array_equal(got[0], wl) and np.array_equal(got[1], wo) and np.array_equal(got[2], wf), world
+    got = D.loopback_dist_all_positions(data, 2, "leftmost")
+    assert np.array_equal(got[0], ws) and np.array_equal(got[1], wln)
+    big = workloads.iid_dna(100_000, 42).copy()
+    for dst in rng.choice(big.size // 32 - 1, 2500, replace=False) * 32:  # one 16-mer in 2500 places
+        big[dst:dst + 16] = np.frombuffer(b"ACGTTGCAACGTTGCA", np.uint8)
+    assert D.loopback_dist_all_positions(big, 2, "all") is None
+
+
 def test_distributed_suffix_sort_more_ranks_than_buckets():
     # n = 10000 -> 3 position buckets: with 5 or 7 ranks some position shards
     # (and SA segments) are empty, between non-empty ones; the halo comes from
