@@ -49,6 +49,16 @@ struct Cand {
     }
 };
 
+// Compact candidates as two shared arrays (starts, lengths): the window walks
+// read lengths of neighbouring entries, 4-byte words in consecutive banks
+// (the interleaved uint2 layout put two entries per bank pair: 2-way conflicts).
+struct CandSoA {
+    const unsigned *st, *ln;
+    __device__ __forceinline__ unsigned start(unsigned t) const { return st[t]; }
+    __device__ __forceinline__ unsigned len(unsigned t) const { return ln[t]; }
+    __device__ __forceinline__ int end(unsigned t) const { return (int)(st[t] + ln[t]) - 1; }
+};
+
 // Per-tile candidate range.  Tiles cover positions [kb + g*G, kb + g*G + G - 1] ∩ [kb, ke].
 // Compact: lo = first t with end_t >= kfirst, hi = #{t : start_t <= klast}.
 // Raw:     lo = first i in [1, kfirst] with i + raw[i] - 1 >= kfirst (else kfirst + 1),
@@ -99,8 +109,8 @@ __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict
 // candidate fills the positions where it is the boundary -- O(tile +
 // candidates), no searches -- unless candidates are few and long
 // (repetitive text), then one binary search per position.
-template <bool RAW, typename IdxT>
-__device__ __forceinline__ void fill_windows(const Cand<RAW> &c, unsigned cnt, int tile_k0, int tile_k1, int npos,
+template <typename C, typename IdxT>
+__device__ __forceinline__ void fill_windows(const C &c, unsigned cnt, int tile_k0, int tile_k1, int npos,
                                              IdxT *s_lo, IdxT *s_hi) {
     if (cnt * 8 < (unsigned)npos) {
         for (int p = threadIdx.x; p < npos; p += kNT) {
@@ -145,6 +155,8 @@ struct TileCtx {
     int npos, out_off;
     IdxT *s_lo, *s_hi;
     unsigned *s_cnt, *s_warp;
+    unsigned short *s_ties;  // tile-local tie list (candidate indices), or null
+    unsigned ties_cap;       // its capacity
     u64 *s_base;
     long long *out0, *out1, *flat;
     u64 *status;
@@ -154,22 +166,20 @@ struct TileCtx {
 // Everything after staging.  Inlined twice (candidates in shared memory or,
 // for oversized windows, in global memory) so each copy uses the right
 // address space (LDS instead of generic loads).
-template <bool RAW, bool ALL, typename IdxT>
-__device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<IdxT> &x) {
+template <typename C, bool ALL, typename IdxT>
+__device__ __forceinline__ void query_tile(const C &c, const TileCtx<IdxT> &x) {
     const unsigned cnt = (unsigned)x.cnt;
-    fill_windows<RAW, IdxT>(c, cnt, (int)x.tile_k0, (int)x.tile_k1, x.npos, x.s_lo, x.s_hi);
+    fill_windows<C, IdxT>(c, cnt, (int)x.tile_k0, (int)x.tile_k1, x.npos, x.s_lo, x.s_hi);
 
     // ---- per position (lane-interleaved: consecutive threads, consecutive positions) ----
     // Windows of up to 32 candidates (the common case) record their ties as a
     // bit mask relative to the window start while finding the maximum, so the
     // tie starts are later read by iterating set bits (nt steps) instead of
     // re-walking the window; longer windows (repetitive text) re-walk.
-    unsigned best[kPPT];
-    unsigned tmask[kPPT];  // tie mask; 0 with best > 0 means "re-walk"
+    unsigned tmask[kPPT];  // tie mask; 0 with ties means "re-walk"
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
         const int p = threadIdx.x + j * kNT;
-        best[j] = 0;
         tmask[j] = 0;
         if (p >= x.npos) continue;
         const unsigned wl = x.s_lo[p], wh = x.s_hi[p];
@@ -207,7 +217,6 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<Idx
                 }
             }
         }
-        best[j] = bl;
         if (ALL) {
             x.out0[x.slot0 + p] = bl;
             x.s_cnt[p] = bl ? nt : 0;
@@ -235,6 +244,17 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<Idx
     }
     unsigned excl;
     const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, x.s_warp);
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x * kPPT + j;
+        if (p < x.npos) x.s_cnt[p] = excl;
+        excl += mine[j];
+    }
+    __syncthreads();
+    // Warp 0 resolves the tile's global base (decoupled look-back) while the
+    // other warps already list the tile's ties in shared memory as candidate
+    // indices in output order; after the barrier the list is written out
+    // coalesced.  Tiles whose ties overflow the list write directly.
     if (threadIdx.x < 32) {
         u64 base = lookback_warp(x.status, x.tile, (u64)block_total, OpSum());
         if (threadIdx.x == 0) {
@@ -242,11 +262,32 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<Idx
             if (x.tile == x.tiles - 1) *x.total_out = base + block_total;
         }
     }
+    const bool staged = x.s_ties != nullptr && block_total <= x.ties_cap;
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x * kPPT + j;
-        if (p < x.npos) x.s_cnt[p] = excl;
-        excl += mine[j];
+        const int p = threadIdx.x + j * kNT;
+        if (!staged || p >= x.npos) continue;
+        const unsigned ex = x.s_cnt[p];
+        const unsigned nxt = (p + 1 < x.npos) ? x.s_cnt[p + 1] : block_total;
+        if (nxt == ex) continue;
+        const unsigned wl = x.s_lo[p];
+        unsigned tm = tmask[j];
+        unsigned w = ex;
+        if (tm) {
+            do {
+                const unsigned b = __ffs(tm) - 1;
+                tm &= tm - 1;
+                x.s_ties[w++] = (unsigned short)(wl + b);
+            } while (tm);
+        } else {
+            const unsigned wh = x.s_hi[p];
+            unsigned bl = 0;  // long window (> 32): maximum again, then the ties
+#pragma unroll 1
+            for (unsigned t = wl; t < wh; ++t) bl = max(bl, c.len(t));
+#pragma unroll 1
+            for (unsigned t = wl; t < wh; ++t)
+                if (c.len(t) == bl) x.s_ties[w++] = (unsigned short)t;
+        }
     }
     __syncthreads();
     const u64 tile_base = *x.s_base;
@@ -257,16 +298,29 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<Idx
         }
         x.out1[x.out_off] = 0;  // offsets of the first position
     }
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) {
+        const int p = threadIdx.x + j * kNT;
+        if (p < x.npos)  // offsets[k+1] = inclusive prefix
+            x.out1[x.slot0 + 1 + p] = (long long)(tile_base + ((p + 1 < x.npos) ? x.s_cnt[p + 1] : block_total));
+    }
     const bool cap_ok = (long long)(tile_base + block_total) <= x.flat_cap;
     long long *const flat_tile = x.flat + tile_base;
+    if (staged) {
+        if (cap_ok) {
+            for (unsigned i = threadIdx.x; i < block_total; i += kNT) flat_tile[i] = c.start(x.s_ties[i]);
+        } else {
+            for (unsigned i = threadIdx.x; i < block_total; i += kNT)
+                if ((long long)(tile_base + i) < x.flat_cap) flat_tile[i] = c.start(x.s_ties[i]);
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
         const int p = threadIdx.x + j * kNT;
         if (p >= x.npos) continue;
         const unsigned ex = x.s_cnt[p];
-        const unsigned nxt = (p + 1 < x.npos) ? x.s_cnt[p + 1] : block_total;
-        x.out1[x.slot0 + 1 + p] = (long long)(tile_base + nxt);  // offsets[k+1] = inclusive prefix
-        const unsigned nt = nxt - ex;
+        const unsigned nt = ((p + 1 < x.npos) ? x.s_cnt[p + 1] : block_total) - ex;
         if (nt == 0) continue;
         const unsigned wl = x.s_lo[p];
         unsigned tm = tmask[j];
@@ -289,8 +343,10 @@ __device__ __forceinline__ void query_tile(const Cand<RAW> &c, const TileCtx<Idx
             } while (tm);
             continue;
         }
-        const unsigned bl = best[j];
         const unsigned wh = x.s_hi[p];
+        unsigned bl = 0;
+#pragma unroll 1
+        for (unsigned t = wl; t < wh; ++t) bl = max(bl, c.len(t));
 #pragma unroll 1
         for (unsigned t = wl; t < wh; ++t) {
             if (c.len(t) == bl) {
@@ -340,6 +396,8 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     x.s_hi = x.s_lo + kG;                                       // window end (exclusive)
     x.s_cnt = x.s_hi + kG;                                      // tie counts -> exclusive offsets
     x.s_warp = s_warp;
+    x.s_ties = nullptr;  // candidates may be > 2^16: direct tie stores
+    x.ties_cap = 0;
     x.s_base = &s_base;
     x.out0 = out0;
     x.out1 = out1;
@@ -374,11 +432,11 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
         mbar_wait(&s_bar, 0);
         c.e = RAW ? nullptr : reinterpret_cast<const uint2 *>(s_stage) + (lo - a);
         c.r = RAW ? reinterpret_cast<const unsigned *>(s_stage) + (lo - a) : nullptr;
-        query_tile<RAW, ALL>(c, x);
+        query_tile<Cand<RAW>, ALL>(c, x);
     } else {
         c.e = RAW ? nullptr : e + lo;
         c.r = RAW ? raw + lo : nullptr;
-        query_tile<RAW, ALL>(c, x);
+        query_tile<Cand<RAW>, ALL>(c, x);
     }
 }
 
@@ -391,16 +449,20 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
 // memory (block scan, order kept) and runs the compact walk on that list --
 // the global LLRc is never written nor read back.  The host only takes this
 // path when every tile's raw range fits the stage (short repeats).
-constexpr int kFStage = kG + 1024 + 16;  // staged raw values incl. alignment slack and slot lo-1
+constexpr int kFStage = kG + 768 + 16;  // staged raw values incl. alignment slack and slot lo-1
 constexpr int kFRawBytes = ((4 * kFStage + 127) / 128) * 128;
 // the raw stage is dead after compaction: the per-position window bounds
-// (u16) and tie counts reuse it -> ~25 KB per CTA, 8 CTAs per SM
-static_assert(2 * 2 * kG + 4 * kG <= kFRawBytes, "window bounds + counts must fit the raw stage");
-static_assert(kFStage < 65536, "u16 window bounds");
-constexpr int kFusedSmem = kFRawBytes + 8 * kFStage;
+// (u16) and tie counts reuse it (region A); then the compacted starts and
+// lengths (B) and the tile's tie list (C, u16 candidate indices: ~2.2 ties
+// per position of headroom over i.i.d. DNA's 1.9) -> 27.5 KB, 8 CTAs per SM
+constexpr int kFRegionA = kFRawBytes > 8 * kG ? kFRawBytes : 8 * kG;
+constexpr int kFTiesCap = 2688;
+static_assert(kFStage < 65536, "u16 window bounds and tie indices");
+constexpr int kFusedSmem = kFRegionA + 8 * kFStage + 2 * kFTiesCap;
+static_assert(kFusedSmem + 128 <= 233472 / 8 - 1024, "8 CTAs per SM");
 
 template <bool ALL>
-__global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict__ raw, long long kb, long long ke,
+__global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restrict__ raw, long long kb, long long ke,
                                                      const long long *__restrict__ bounds, int out_off,
                                                      long long *__restrict__ out0, long long *__restrict__ out1,
                                                      long long *__restrict__ flat, long long flat_cap,
@@ -408,7 +470,8 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
                                                      unsigned long long *total_out) {
     extern __shared__ __align__(128) unsigned char dsm[];
     unsigned *s_raw = reinterpret_cast<unsigned *>(dsm);
-    uint2 *s_list = reinterpret_cast<uint2 *>(dsm + kFRawBytes);
+    unsigned *s_st = reinterpret_cast<unsigned *>(dsm + kFRegionA);  // compacted starts
+    unsigned *s_ln = s_st + kFStage;                                   // compacted lengths
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ unsigned s_tile;
     __shared__ unsigned s_warp[kNT / 32];
@@ -436,6 +499,8 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
     x.s_hi = x.s_lo + kG;
     x.s_cnt = reinterpret_cast<unsigned *>(dsm + 4 * kG);
     x.s_warp = s_warp;
+    x.s_ties = reinterpret_cast<unsigned short *>(dsm + kFRegionA + 8 * kFStage);
+    x.ties_cap = kFTiesCap;
     x.s_base = &s_base;
     x.out0 = out0;
     x.out1 = out1;
@@ -466,7 +531,10 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
     const unsigned cnt = block_exclusive_sum<kNT>(nf, w, s_warp);
     for (int q = 0; q < per; ++q) {
         const int o = o0 + q;
-        if (o < nr && r0[o] > 0u && r0[o] >= r0[o - 1]) s_list[w++] = make_uint2((unsigned)(lo + o), r0[o]);
+        if (o < nr && r0[o] > 0u && r0[o] >= r0[o - 1]) {
+            s_st[w] = (unsigned)(lo + o);
+            s_ln[w++] = r0[o];
+        }
     }
     x.cnt = cnt;
     __syncthreads();  // s_raw dead from here: the window bounds take its place
@@ -475,11 +543,10 @@ __global__ void __launch_bounds__(kNT) k_query_fused(const unsigned *__restrict_
         x.s_hi[i] = 0;
     }
     __syncthreads();
-    Cand<false> c;
-    c.e = s_list;
-    c.r = nullptr;
-    c.base = 0;
-    query_tile<false, ALL>(c, x);
+    CandSoA c;
+    c.st = s_st;
+    c.ln = s_ln;
+    query_tile<CandSoA, ALL>(c, x);
 }
 
 // max over tiles of the staged raw range (hi - lo + 8) -> *out
@@ -540,7 +607,7 @@ __global__ void __launch_bounds__(kNT) k_steps(const uint2 *__restrict__ e, cons
         c.e = RAW ? nullptr : e + lo;
         c.r = RAW ? raw + lo : nullptr;
     }
-    fill_windows<RAW, unsigned>(c, (unsigned)(cnt > 0 ? cnt : 0), (int)tile_k0, (int)(tile_k0 + npos - 1), npos, s_lo, s_hi);
+    fill_windows<Cand<RAW>, unsigned>(c, (unsigned)(cnt > 0 ? cnt : 0), (int)tile_k0, (int)(tile_k0 + npos - 1), npos, s_lo, s_hi);
     unsigned long long mn = ~0ull, mx = 0, sum = 0, n = 0;
     for (int p = threadIdx.x; p < npos; p += kNT) {
         const long long w = (long long)s_hi[p] - (long long)s_lo[p];

@@ -5,6 +5,7 @@ usage: python tools/ncu_lines.py report.ncu-rep [file-substring] [top]
 import csv
 import io
 import subprocess
+import os
 import sys
 
 
@@ -40,7 +41,8 @@ def main():
     ti = sum(r[2] for r in rows) or 1
     ts = sum(r[3] for r in rows) or 1
     print(f"total warp-inst {ti:,}  samples {ts:,}")
-    for r in sorted(rows, key=lambda r: -r[2])[:top]:
+    key = 3 if os.environ.get("BY_STALL") else 2
+    for r in sorted(rows, key=lambda r: -r[key])[:top]:
         print(f"{r[0]}:{r[1]:<5} inst {100 * r[2] / ti:5.1f}%  stall {100 * r[3] / ts:5.1f}%  {r[4]}")
 
 
