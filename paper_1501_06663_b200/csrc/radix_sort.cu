@@ -195,11 +195,43 @@ __global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3)
         __syncthreads();
         mbar_wait(&sm.bar, 0);
     }
+    // u32 keys from the packed text: a tile past the short suffixes covers
+    // consecutive positions, so its bit range of the stream is staged once in
+    // shared memory as 32-bit MSB-first chunks (through the still unused
+    // exchange buffer) and each key is one funnel shift of two chunks.
+    bool text_fast = false;
+    if (TEXT && sizeof(KeyT) == 4 && tbase >= tk.S && tk.b * tk.K <= 32) {
+        text_fast = true;
+        unsigned *chunk = reinterpret_cast<unsigned *>(sm.x.keys);
+        const long long p0 = tbase - tk.S;
+        const long long q0 = ((long long)tk.b * p0) >> 5;
+        const int nch = (int)((((long long)tk.b * (p0 + tile_count - 1)) >> 5) + 2 - q0);  // <= 8 kTile / 32 + 2
+        for (int j = threadIdx.x; j < nch; j += kNT) {
+            const long long q = q0 + j;
+            const u64 w = tk.stream[q >> 1];
+            chunk[j] = (q & 1) ? (unsigned)w : (unsigned)(w >> 32);
+        }
+        __syncthreads();
+        const unsigned off0 = (unsigned)((long long)tk.b * p0 - 32 * q0);
+        const int kb = tk.b * tk.K;
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) {
-        const int o = wbase + i * 32;
-        if (o < tile_count)
-            k[i] = TEXT ? (KeyT)text_key(tk, text_pos(tk, tbase + o)) : kTma ? sm.x.keys[o] : keys_in[tbase + o];
+        for (int i = 0; i < kIPT; ++i) {
+            const int o = wbase + i * 32;
+            if (o < tile_count) {
+                const unsigned bit = off0 + (unsigned)(tk.b * o);
+                const unsigned j = bit >> 5;
+                const unsigned x = __funnelshift_l(chunk[j + 1], chunk[j], bit & 31);
+                k[i] = (KeyT)(kb >= 32 ? x : x >> (32 - kb));
+            }
+        }
+    }
+    if (!text_fast) {
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i) {
+            const int o = wbase + i * 32;
+            if (o < tile_count)
+                k[i] = TEXT ? (KeyT)text_key(tk, text_pos(tk, tbase + o)) : kTma ? sm.x.keys[o] : keys_in[tbase + o];
+        }
     }
     // 1) tile digit histogram first, published right away (decoupled
     //    look-back: successors can use this tile's aggregate while it is still
