@@ -18,6 +18,7 @@
 // look-back for the tile's global CSR base -> offsets and tie starts written
 // directly in the reference int64 layout.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
                                                      long long *__restrict__ out0, long long *__restrict__ out1,
                                                      long long *__restrict__ flat, long long flat_cap,
                                                      unsigned *counter, u64 *status, long long tiles,
-                                                     unsigned long long *total_out) {
+                                                     unsigned long long *total_out, unsigned ties_cap) {
     extern __shared__ __align__(128) unsigned char dsm[];
     unsigned *s_raw = reinterpret_cast<unsigned *>(dsm);
     unsigned *s_st = reinterpret_cast<unsigned *>(dsm + kFRegionA);  // compacted starts
@@ -500,7 +501,7 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
     x.s_cnt = reinterpret_cast<unsigned *>(dsm + 4 * kG);
     x.s_warp = s_warp;
     x.s_ties = reinterpret_cast<unsigned short *>(dsm + kFRegionA + 8 * kFStage);
-    x.ties_cap = kFTiesCap;
+    x.ties_cap = ties_cap;
     x.s_base = &s_base;
     x.out0 = out0;
     x.out1 = out1;
@@ -705,7 +706,7 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     if (!all) {
         if (fused)
             RS_LAUNCH_B(c, qbytes, (k_query_fused<false>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
-                        out_off, out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
+                        out_off, out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot, 0u);
         else if (rawp)
             RS_LAUNCH_B(c, qbytes, (k_query<true, false>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,
                       out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot);
@@ -724,9 +725,17 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     for (int attempt = 0; attempt < 3; ++attempt) {
         long long *flat = (long long *)buf(c, B_FLAT, sizeof(long long) * cap_slots);
         Scratch s = scratch(c, tiles);
-        if (fused)
+        if (fused) {
+            // RS_FUSED_TIES_CAP (tests only) shrinks the shared tie list so
+            // the direct-store fallback of overflowing tiles gets exercised
+            unsigned ties_cap = kFTiesCap;
+            if (const char *e = std::getenv("RS_FUSED_TIES_CAP")) {
+                const long v = std::strtol(e, nullptr, 10);
+                if (v >= 0 && v < ties_cap) ties_cap = (unsigned)v;
+            }
             RS_LAUNCH_B(c, qbytes, (k_query_fused<true>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
-                        out_off, out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot);
+                        out_off, out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot, ties_cap);
+        }
         else if (rawp)
             RS_LAUNCH_B(c, qbytes, (k_query<true, true>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,
                       out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot);

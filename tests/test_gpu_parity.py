@@ -207,6 +207,19 @@ def test_tile_boundaries_and_long_windows():
             assert all(np.array_equal(a, b) for a, b in zip(arrs, want)), (path, mode)
 
 
+@pytest.mark.parametrize("cap", ["0", "1", "1500", "2000"])
+def test_fused_scan_tie_list_overflow(cap, monkeypatch):
+    # the fused all-ties scan lists a tile's ties in shared memory (2688 of
+    # them) and stores overflowing tiles directly; shrink the list so both
+    # paths, mixed within one launch, are checked against the oracle
+    monkeypatch.setenv("RS_FUSED_TIES_CAP", cap)
+    for data in (workloads.iid_dna(300_000, 11), workloads.make("C2", 1 << 18)):
+        want = oracle.all_positions(data, mode="all", path="compact", workers=4)
+        A = rb.all_positions(rb.Text(data), mode="all", path="compact")
+        assert np.array_equal(A.lengths, want[0]) and np.array_equal(A.offsets, want[1]), cap
+        assert np.array_equal(A.flat_starts, want[2]), cap
+
+
 def test_api_errors():
     with pytest.raises(ValueError):
         rb.all_positions(rb.Text.from_str("abc"), mode="bogus")
