@@ -220,6 +220,40 @@ def test_fused_scan_tie_list_overflow(cap, monkeypatch):
         assert np.array_equal(A.flat_starts, want[2]), cap
 
 
+@pytest.mark.parametrize("config", ["C2", "C3", "C4"])
+def test_full_size_properties(config):
+    # BASELINE configs at full size (64 Mi planted DNA, the 256 Mi headline,
+    # 100 Mi English-like), beyond what the oracle finishes quickly: the structures are verified on device by
+    # direct comparison, the raw and compact paths (different kernels) must
+    # agree array for array, leftmost must equal the first tie,
+    # and every tie start must cover its position with the position's length,
+    # blocks strictly increasing.
+    data = workloads.make(config)
+    n = data.size
+    t = rb.Text(data)
+    s = rb.build_suffix_structures(t)
+    assert rb.verify_suffix_structures(t, s)
+    A = rb.all_positions(t, mode="all", path="compact", structures=s)
+    R = rb.all_positions(t, mode="all", path="raw", structures=s)
+    assert np.array_equal(A.lengths, R.lengths) and np.array_equal(A.offsets, R.offsets)
+    assert np.array_equal(A.flat_starts, R.flat_starts)
+    del R
+    L = rb.all_positions(t, mode="leftmost", path="compact", structures=s)
+    del s
+    assert np.array_equal(L.lengths, A.lengths)
+    cnt = np.diff(A.offsets)[1:]
+    has = cnt > 0
+    assert np.array_equal(has, A.lengths[1:] > 0)
+    assert np.array_equal(L.starts[1:][has], A.flat_starts[A.offsets[1:-1][has]])
+    assert (L.starts[1:][~has] == -1).all() and L.starts[0] == -1
+    del L
+    k = np.repeat(np.arange(1, n + 1, dtype=np.int64), cnt)
+    st = A.flat_starts
+    assert ((st <= k) & (k <= st + np.repeat(A.lengths[1:], cnt) - 1)).all()
+    same = k[1:] == k[:-1]
+    assert (st[1:][same] > st[:-1][same]).all()
+
+
 def test_api_errors():
     with pytest.raises(ValueError):
         rb.all_positions(rb.Text.from_str("abc"), mode="bogus")
