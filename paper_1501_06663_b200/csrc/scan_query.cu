@@ -478,14 +478,12 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
     __shared__ unsigned s_warp[kNT / 32];
     __shared__ u64 s_base;
 
-    long long tile;
-    if (ALL) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
-        __syncthreads();
-        tile = s_tile;
-    } else {
-        tile = blockIdx.x;
-    }
+    // tile = blockIdx.x also for the look-back of the all variant (blocks
+    // are dispatched in index order, as CUB's single-pass scan relies on):
+    // saves the tile counter's round trip before the bounds load and TMA
+    (void)counter;
+    (void)s_tile;
+    const long long tile = blockIdx.x;
     TileCtx<unsigned short> x;
     x.tile = tile;
     const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];  // raw slots [lo, hi)
