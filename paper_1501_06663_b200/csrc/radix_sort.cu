@@ -170,9 +170,13 @@ __global__ void __launch_bounds__(kNT, sizeof(KeyT) == 4 ? 4 : 3)
         for (int i = threadIdx.x; i < kWarps * kRadix / 2; i += kNT) wc[i] = 0;
     }
     sm.hist[threadIdx.x] = 0;
-    if (threadIdx.x == 0) sm.tile_id = atomicAdd(counter, 1u);
+    // u64 passes: tile = blockIdx.x (blocks are dispatched in index order, as
+    // CUB's single-pass scan relies on), no tile-counter round trip before the
+    // TMA loads (C4 sort 14.3 -> 13.7 ms).  u32 passes keep the dynamic tile
+    // counter (measured 5.08 vs 5.31 ms per 3 passes with blockIdx.x).
+    if (sizeof(KeyT) == 4 && threadIdx.x == 0) sm.tile_id = atomicAdd(counter, 1u);
     __syncthreads();
-    const unsigned tile = sm.tile_id;
+    const unsigned tile = sizeof(KeyT) == 4 ? sm.tile_id : blockIdx.x;
     const long long tbase = (long long)tile * kTile;
     const int tile_count = count - tbase < kTile ? (int)(count - tbase) : kTile;
     const int wbase = warp * (kIPT * 32) + lane;  // item i of this thread: tile offset wbase + 32 i
