@@ -120,6 +120,15 @@ int rs_set_structures(rs_ctx *ctx, const int64_t *sa, const int64_t *rank, const
  * (size and sentinel checks are the caller's, as in the reference). */
 int rs_verify_structures(rs_ctx *ctx, const uint8_t *text, int64_t n, const int64_t *sa,
                          const int64_t *rank, const int64_t *lcp, int64_t *ok);
+/* Independent check of query answers against compact entries starts/lengths[m]
+ * (the reference's Algorithm 4 as written, _kernels_numba.py:74-85 +
+ * :158-195: binary search + forward walk per position, no code shared with
+ * the scan kernels).  All-ties arrays (a_lengths[n+1], a_offsets[n+2],
+ * a_flat[total]) and/or leftmost arrays (l_starts/l_lengths[n+1]) may be
+ * NULL.  *bad receives the number of positions whose answer differs. */
+int rs_check_answers(rs_ctx *ctx, const int64_t *starts, const int64_t *lengths, int64_t m, int64_t n,
+                     const int64_t *a_lengths, const int64_t *a_offsets, const int64_t *a_flat,
+                     int64_t total, const int64_t *l_starts, const int64_t *l_lengths, int64_t *bad);
 /* query.py:234 build_suffix_structures on device from the loaded text. */
 int rs_build_structures(rs_ctx *ctx);
 int rs_get_structures(rs_ctx *ctx, int64_t *sa, int64_t *rank, int64_t *lcp);

@@ -272,3 +272,130 @@ def summarize_steps(steps: np.ndarray):
     if covered.size == 0:
         return 0, 0, 0.0, 0
     return int(covered.min()), int(covered.max()), float(covered.mean()), int(covered.size)
+
+
+# -- oracle32.c: u32 restatement for full-size digests ---------------------------
+_lib32 = None
+_O32_FIELDS = ("sa", "rank", "lcp", "raw", "flags", "c_starts", "c_lengths")
+
+
+def _load32():
+    global _lib32
+    if _lib32 is not None:
+        return _lib32
+    path = _HERE / "liboracle32.so"
+    if not path.exists():
+        build()
+    lib = ctypes.CDLL(str(path))
+    i64, c_int, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    sig = {
+        "o32_create": (vp, [_U8P, i64]),
+        "o32_destroy": (None, [vp]),
+        "o32_sa": (c_int, [vp]),
+        "o32_lcp": (c_int, [vp]),
+        "o32_raw": (c_int, [vp]),
+        "o32_free_structures": (None, [vp]),
+        "o32_compact": (i64, [vp]),
+        "o32_chunk": (c_int, [vp, c_int, i64, i64, _I64P]),
+        "o32_leftmost": (None, [vp, i64, i64, _I64P, _I64P]),
+        "o32_all_count": (None, [vp, i64, i64, _I64P, _I64P]),
+        "o32_all_fill": (None, [vp, i64, i64, _I64P, _I64P, _I64P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib32 = lib
+    return lib
+
+
+def digests32(data: np.ndarray, chunk: int = 1 << 24, log=None) -> dict:
+    """sha256 digests (16 hex) of every int64 reference-layout array of the
+    compact path (sa, rank, lcp, raw, flags, ps, c_starts, c_lengths,
+    l_starts, l_lengths, a_lengths, a_offsets, a_flat) plus n, m, T, max_llr,
+    computed by oracle32.c with uint32 indices and streamed in chunks."""
+    import hashlib
+    import time
+    lib = _load32()
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    n = int(data.size)
+    log = log or (lambda s: None)
+    h = lib.o32_create(_u8(data), n)
+    if not h:
+        raise MemoryError("o32_create")
+    out = {}
+    try:
+        t0 = time.time()
+        rounds = lib.o32_sa(h)
+        if rounds < 0:
+            raise MemoryError("o32_sa")
+        log(f"suffix array: {rounds} doubling rounds, {time.time() - t0:.1f} s")
+        if lib.o32_lcp(h) != 0 or lib.o32_raw(h) != 0:
+            raise MemoryError("o32_lcp/o32_raw")
+        log(f"lcp + raw: {time.time() - t0:.1f} s")
+        m = int(lib.o32_compact(h))
+        if m < 0:
+            raise MemoryError("o32_compact")
+        out.update(n=n, m=m, sa_rounds=int(rounds))
+        buf = np.empty(chunk, np.int64)
+        sizes = {"sa": n + 1, "rank": n + 1, "lcp": n + 2, "raw": n + 1, "flags": n + 1,
+                 "c_starts": m, "c_lengths": m}
+        max_llr = 0
+        for w, f in enumerate(_O32_FIELDS):
+            hs = hashlib.sha256()
+            hps = hashlib.sha256() if f == "flags" else None
+            carry = 0
+            for lo in range(0, sizes[f], chunk):
+                cnt = min(chunk, sizes[f] - lo)
+                lib.o32_chunk(h, w, lo, cnt, _p(buf))
+                v = buf[:cnt]
+                hs.update(v.tobytes())
+                if f == "raw":
+                    max_llr = max(max_llr, int(v.max(initial=0)))
+                if hps is not None:  # ps = inclusive scan of flags, ps[0] = 0 (llr.py:92-96)
+                    ps = np.cumsum(v) + carry
+                    carry = int(ps[-1])
+                    hps.update(ps.tobytes())
+            out[f] = hs.hexdigest()[:16]
+            if hps is not None:
+                out["ps"] = hps.hexdigest()[:16]
+            if f == "raw":
+                lib.o32_free_structures(h)
+        out["max_llr"] = max_llr
+        log(f"structures/llr digests: {time.time() - t0:.1f} s")
+        # leftmost (query.py:171-184): starts[0] = -1, lengths[0] = 0
+        hs, hl = hashlib.sha256(), hashlib.sha256()
+        hs.update(np.array([-1], np.int64).tobytes())
+        hl.update(np.array([0], np.int64).tobytes())
+        s_buf, l_buf = np.empty(chunk, np.int64), np.empty(chunk, np.int64)
+        for lo in range(1, n + 1, chunk):
+            hi = min(lo + chunk, n + 1)
+            lib.o32_leftmost(h, lo, hi, _p(s_buf), _p(l_buf))
+            hs.update(s_buf[:hi - lo].tobytes())
+            hl.update(l_buf[:hi - lo].tobytes())
+        out.update(l_starts=hs.hexdigest()[:16], l_lengths=hl.hexdigest()[:16])
+        log(f"leftmost: {time.time() - t0:.1f} s")
+        # all ties (query.py:187-215): lengths[0] = 0, offsets[0] = offsets[1] = 0
+        hl, ho, hf = hashlib.sha256(), hashlib.sha256(), hashlib.sha256()
+        hl.update(np.array([0], np.int64).tobytes())
+        ho.update(np.array([0, 0], np.int64).tobytes())
+        cnt_buf = np.empty(chunk, np.int64)
+        base = 0
+        for lo in range(1, n + 1, chunk):
+            hi = min(lo + chunk, n + 1)
+            c = hi - lo
+            lib.o32_all_count(h, lo, hi, _p(l_buf), _p(cnt_buf))
+            incl = np.cumsum(cnt_buf[:c])
+            local = np.ascontiguousarray(incl - cnt_buf[:c])
+            flat = np.empty(int(incl[-1]), np.int64)
+            lib.o32_all_fill(h, lo, hi, _p(l_buf), _p(local), _p(flat))
+            hl.update(l_buf[:c].tobytes())
+            ho.update((incl + base).tobytes())
+            hf.update(flat.tobytes())
+            base += int(incl[-1])
+        out.update(T=base, a_lengths=hl.hexdigest()[:16], a_offsets=ho.hexdigest()[:16],
+                   a_flat=hf.hexdigest()[:16])
+        log(f"all ties: {time.time() - t0:.1f} s")
+    finally:
+        lib.o32_destroy(h)
+    return out

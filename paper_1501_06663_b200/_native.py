@@ -56,6 +56,8 @@ SIGNATURES = {
     "rs_build_structures": [_CTX],
     "rs_verify_structures": [_CTX, _U8P, ctypes.c_int64, _I64P, _I64P, _I64P, _I64P],
     "rs_get_structures": [_CTX, _I64P, _I64P, _I64P],
+    "rs_check_answers": [_CTX, _I64P, _I64P, ctypes.c_int64, ctypes.c_int64, _I64P, _I64P, _I64P,
+                         ctypes.c_int64, _I64P, _I64P, _I64P],
     "rs_set_raw": [_CTX, _I64P, ctypes.c_int64],
     "rs_set_compact": [_CTX, _I64P, _I64P, ctypes.c_int64, ctypes.c_int64],
     "rs_query": [_CTX, ctypes.c_int, ctypes.c_int, _I64P],

@@ -23,6 +23,9 @@ void flags_i64(rs_ctx *c, const long long *d_raw, long long n, long long *d_out)
 void scan_i64(rs_ctx *c, const long long *d_in, long long count, long long *d_out);
 void scatter_i64(rs_ctx *c, const long long *d_raw, const long long *d_flags, const long long *d_ps,
                  long long n, long long m, long long *d_starts, long long *d_lengths);
+long long check_answers(rs_ctx *c, const long long *d_cs, const long long *d_cl, long long m, long long n,
+                        const long long *d_L, const long long *d_O, const long long *d_F, long long T,
+                        const long long *d_ls, const long long *d_ll);
 bool verify_structures(rs_ctx *c, const unsigned char *d_text, long long n, const long long *d_sa,
                        const long long *d_rank, const long long *d_lcp);
 long long serialize_tsv(rs_ctx *c, int mode, long long lo, long long hi);
@@ -560,6 +563,37 @@ int rs_verify_structures(rs_ctx *c, const uint8_t *text, int64_t n, const int64_
         h2d(c, drk, rank, 8 * (size_t)(n + 1));
         h2d(c, dlc, lcp, 8 * (size_t)(n + 2));
         *ok = verify_structures(c, dt, n, dsa, drk, dlc) ? 1 : 0;
+    });
+}
+
+int rs_check_answers(rs_ctx *c, const int64_t *starts, const int64_t *lengths, int64_t m, int64_t n,
+                     const int64_t *a_lengths, const int64_t *a_offsets, const int64_t *a_flat, int64_t total,
+                     const int64_t *l_starts, const int64_t *l_lengths, int64_t *bad) {
+    return guarded(c, [&] {
+        check_n(n);
+        if (m < 0 || m > n || total < 0) fail(RS_EINVAL, "bad entry count or tie total");
+        invalidate(c);
+        *bad = 0;
+        long long *dcs = (long long *)buf(c, B_I64A, 8 * (size_t)(m + 1));
+        long long *dcl = (long long *)buf(c, B_I64B, 8 * (size_t)(m + 1));
+        h2d(c, dcs, starts, 8 * (size_t)m);
+        h2d(c, dcl, lengths, 8 * (size_t)m);
+        long long *dL = nullptr, *dO = nullptr, *dF = nullptr, *dls = nullptr, *dll = nullptr;
+        if (a_lengths) {
+            dL = (long long *)buf(c, B_I64C, 8 * (size_t)(n + 1));
+            dO = (long long *)buf(c, B_I64D, 8 * (size_t)(n + 2));
+            dF = (long long *)buf(c, B_T1, 8 * (size_t)(total + 1));
+            h2d(c, dL, a_lengths, 8 * (size_t)(n + 1));
+            h2d(c, dO, a_offsets, 8 * (size_t)(n + 2));
+            h2d(c, dF, a_flat, 8 * (size_t)total);
+        }
+        if (l_starts) {
+            dls = (long long *)buf(c, B_T2, 8 * (size_t)(n + 1));
+            dll = (long long *)buf(c, B_T3, 8 * (size_t)(n + 1));
+            h2d(c, dls, l_starts, 8 * (size_t)(n + 1));
+            h2d(c, dll, l_lengths, 8 * (size_t)(n + 1));
+        }
+        *bad = check_answers(c, dcs, dcl, m, n, dL, dO, dF, total, dls, dll);
     });
 }
 

@@ -168,6 +168,16 @@ void add_bytes_last(rs_ctx *c, double bytes);
 #define RS_LAUNCH(ctx, kernel, grid, block, smem, ...) \
     RS_LAUNCH_B(ctx, 0, kernel, grid, block, smem, __VA_ARGS__)
 
+// Kernel attributes (cudaFuncSetAttribute) are per device context: run `f`
+// once per call site and device (a process may drive several devices).
+template <typename F>
+inline void once_per_device(unsigned long long &mask, int device, F &&f) {
+    const unsigned long long bit = 1ull << (device & 63);
+    if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return;
+    f();
+    __atomic_fetch_or(&mask, bit, __ATOMIC_RELEASE);
+}
+
 inline unsigned grid_for(long long items, int per_block) {
     long long g = (items + per_block - 1) / per_block;
     return (unsigned)(g < 1 ? 1 : g);
@@ -219,6 +229,17 @@ __device__ __forceinline__ u64 warp_reduce(u64 v, Op op) {
 // Called by ONE full warp of the tile.  Publishes `aggregate` for `tile`,
 // looks back over predecessors and returns the exclusive prefix (identical
 // in every lane).  status[] must be zeroed before the launch.
+//
+// Forward-progress assumption: a tile only waits on LOWER tile ids.  Kernels
+// that take their tile id from an atomic counter (k_scan_i64, k_onesweep on
+// u32 keys, k_compact_raw, ...) are safe under any block scheduling.  Two hot
+// kernels (k_query_fused, k_onesweep on u64 keys) use tile = blockIdx.x to
+// save the counter round trip before their TMA loads; that relies on the
+// hardware dispatching a grid's blocks in increasing linear index, which it
+// does for a whole GPU (measured: every launch in the parity suites and the
+// fuzzers) but which is not a documented guarantee -- do not run those two
+// under MPS / green-context SM partitioning without switching them back to
+// the atomic tile counter.
 template <typename Op>
 __device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op) {
     const int lane = threadIdx.x & 31;
@@ -250,6 +271,62 @@ __device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op) 
         base -= 32;
     }
     if (lane == 0) st_relaxed(&status[tile], kFlagPre | (op(exclusive, aggregate) & kValMask));
+    return exclusive;
+}
+
+// Look-back for full 64-bit payloads (the int64 API scan, engine.py:77-110,
+// whose values may be negative or exceed 2^62).  The flag lives in its own
+// word and each tile has separate aggregate and inclusive slots, each written
+// once before the flag that announces it (release / acquire), so a reader
+// never pairs a flag with a value it does not describe.
+// st layout: flag[tiles] | agg[tiles] | incl[tiles], zeroed before the launch.
+__device__ __forceinline__ void st_release(u64 *p, u64 v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_acquire(const u64 *p) {
+    u64 v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __noinline__ static u64 lookback_warp_wide(u64 *st, long long tiles, long long tile, u64 aggregate) {
+    const int lane = threadIdx.x & 31;
+    u64 *flag = st, *agg = st + tiles, *incl = st + 2 * tiles;
+    if (tile == 0) {
+        if (lane == 0) {
+            st_relaxed(&incl[0], aggregate);
+            st_release(&flag[0], 2);
+        }
+        return 0;
+    }
+    if (lane == 0) {
+        st_relaxed(&agg[tile], aggregate);
+        st_release(&flag[tile], 1);
+    }
+    u64 exclusive = 0;
+    long long base = tile - 1;
+    while (true) {
+        long long idx = base - lane;
+        u64 f = 2, v = 0;
+        if (idx >= 0) {
+            f = ld_acquire(&flag[idx]);
+            while (f == 0) {
+                __nanosleep(20);
+                f = ld_acquire(&flag[idx]);
+            }
+            v = ld_relaxed(f == 2 ? &incl[idx] : &agg[idx]);
+        }
+        unsigned pre = __ballot_sync(0xffffffffu, f == 2);
+        int first = pre ? __ffs(pre) - 1 : 32;
+        v = (lane <= first) ? v : 0;
+        v = warp_reduce(v, OpSum());
+        exclusive += v;
+        if (pre) break;
+        base -= 32;
+    }
+    if (lane == 0) {
+        st_relaxed(&incl[tile], exclusive + aggregate);
+        st_release(&flag[tile], 2);
+    }
     return exclusive;
 }
 

@@ -130,7 +130,7 @@ __global__ void k_flags_i64(const long long *__restrict__ raw, long long n, long
 constexpr int kScanIPT = 8;
 __global__ void __launch_bounds__(kNT) k_scan_i64(const long long *__restrict__ in, long long count,
                                                   long long *__restrict__ out, unsigned *counter,
-                                                  u64 *status) {
+                                                  u64 *status, long long tiles) {
     __shared__ unsigned s_tile;
     __shared__ u64 s_warp[kNT / 32];
     __shared__ u64 s_base;
@@ -148,11 +148,11 @@ __global__ void __launch_bounds__(kNT) k_scan_i64(const long long *__restrict__ 
     u64 excl;
     u64 total = block_exclusive_sum64<kNT>(s, excl, s_warp);
     if (threadIdx.x < 32) {
-        u64 base = lookback_warp(status, tile, total, OpSum());
+        u64 base = lookback_warp_wide(status, tiles, tile, total);
         if (threadIdx.x == 0) s_base = base;
     }
     __syncthreads();
-    u64 acc = s_base + excl;
+    u64 acc = s_base + excl;  // two's-complement wraparound, like np.cumsum on int64
 #pragma unroll
     for (int j = 0; j < kScanIPT; ++j) {
         acc += (u64)v[j];
@@ -359,8 +359,8 @@ void flags_i64(rs_ctx *c, const long long *d_raw, long long n, long long *d_out)
 void scan_i64(rs_ctx *c, const long long *d_in, long long count, long long *d_out) {
     if (count <= 0) return;
     long long tiles = (count + kNT * kScanIPT - 1) / (kNT * kScanIPT);
-    Scratch s = scratch(c, tiles);
-    RS_LAUNCH(c, k_scan_i64, (unsigned)tiles, kNT, 0, d_in, count, d_out, s.counter, s.status);
+    Scratch s = scratch(c, 3 * tiles);
+    RS_LAUNCH(c, k_scan_i64, (unsigned)tiles, kNT, 0, d_in, count, d_out, s.counter, s.status, tiles);
 }
 
 void scatter_i64(rs_ctx *c, const long long *d_raw, const long long *d_flags, const long long *d_ps,

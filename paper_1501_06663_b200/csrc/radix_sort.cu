@@ -398,14 +398,13 @@ void radix_sort_pairs(rs_ctx *c, KeyT *keys, KeyT *keys_alt, unsigned *vals, uns
     fetch_small(c, h.data(), hist, sizeof(unsigned long long) * h.size());
     RS_LAUNCH(c, k_hist_scan, passes, kRadix, 0, hist);
 
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned long long attr_set = 0;
+    once_per_device(attr_set, c->device, [] {
         RS_CUDA(cudaFuncSetAttribute(k_onesweep<false, KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(SortSmem<KeyT>)));
         RS_CUDA(cudaFuncSetAttribute(k_onesweep<true, KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(SortSmem<KeyT>)));
-        attr_set = true;
-    }
+    });
     long long tiles = (count + kTile - 1) / kTile;
     KeyT *kin = keys, *kout = keys_alt;
     unsigned *vin = vals, *vout = vals_alt;

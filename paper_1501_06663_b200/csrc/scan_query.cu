@@ -678,22 +678,20 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
         unsigned long long mx = 0;
         fetch_small(c, &mx, span, sizeof(mx));
         if (mx > (unsigned long long)kFStage) return false;  // long repeats: the caller materialises LLRc
-        static bool fattr = false;
-        if (!fattr) {
+        static unsigned long long fattr = 0;
+        once_per_device(fattr, c->device, [] {
             RS_CUDA(cudaFuncSetAttribute(k_query_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
             RS_CUDA(cudaFuncSetAttribute(k_query_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
-            fattr = true;
-        }
+        });
     }
 
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    once_per_device(attr, c->device, [] {
         RS_CUDA(cudaFuncSetAttribute(k_query<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
         RS_CUDA(cudaFuncSetAttribute(k_query<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
         RS_CUDA(cudaFuncSetAttribute(k_query<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
         RS_CUDA(cudaFuncSetAttribute(k_query<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuerySmem));
-        attr = true;
-    }
+    });
     long long *out0 = (long long *)buf(c, B_OUT0, sizeof(long long) * (size_t)(n_slots + 1));
     long long *out1 = (long long *)buf(c, B_OUT1, sizeof(long long) * (size_t)(n_slots + 2));
     unsigned long long *tot = (unsigned long long *)buf(c, B_SMALL, 4096) + 2;
@@ -765,13 +763,12 @@ void walk_steps(rs_ctx *c, int path, long long n, long long *d_steps, unsigned l
         const long long count = rawp ? 0 : c->m;
         long long tiles = (n + kG - 1) / kG;
         long long *bounds = (long long *)buf(c, B_BOUNDS, sizeof(long long) * 2 * (size_t)tiles);
-        static bool attr = false;
-        if (!attr) {
+        static unsigned long long attr = 0;
+        once_per_device(attr, c->device, [] {
             const int sm = kStageBytes + 2 * 4 * kG;
             RS_CUDA(cudaFuncSetAttribute(k_steps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
             RS_CUDA(cudaFuncSetAttribute(k_steps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-            attr = true;
-        }
+        });
         const int sm = kStageBytes + 2 * 4 * kG;
         if (rawp) {
             RS_LAUNCH(c, k_bounds<true>, grid_for(tiles, 128), 128, 0, d_e, d_raw, count, 1, n, tiles, bounds, 1ll);

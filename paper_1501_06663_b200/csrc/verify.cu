@@ -69,7 +69,65 @@ __global__ void k_check(const unsigned char *__restrict__ text, const long long 
     }
 }
 
+// Independent answer checker (the reference's Algorithm 4 taken literally,
+// _kernels_numba.py:74-85 + :158-195): one thread per position k binary
+// searches the first compact entry whose end reaches k, walks the window
+// forward while start <= k, and checks that the results claim exactly the
+// maximum length over the window (lengths), exactly the entries of that
+// length in increasing start order (offsets, flat) and, when given, the
+// first of them as the leftmost answer.  Shares no code with the scan
+// kernels of scan_query.cu (no window bounds, no staging, no tile lists).
+__global__ void k_check_answers(const long long *__restrict__ cs, const long long *__restrict__ cl,
+                                long long m, long long n, const long long *__restrict__ L,
+                                const long long *__restrict__ O, const long long *__restrict__ F,
+                                long long T, const long long *__restrict__ ls,
+                                const long long *__restrict__ ll, unsigned long long *bad) {
+    long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x + 1;
+    if (k > n) return;
+    long long lo = 0, hi = m;
+    while (lo < hi) {
+        long long mid = (lo + hi) >> 1;
+        if (cs[mid] + cl[mid] - 1 < k) lo = mid + 1; else hi = mid;
+    }
+    long long best = 0, first = -1;
+    for (long long t = lo; t < m && cs[t] <= k; ++t)
+        if (cl[t] > best) { best = cl[t]; first = cs[t]; }
+    bool ok = true;
+    if (L) {
+        ok = L[k] == best;
+        long long o0 = O[k], o1 = O[k + 1];
+        ok = ok && 0 <= o0 && o0 <= o1 && o1 <= T;
+        if (ok) {
+            long long idx = o0;
+            if (best > 0)
+                for (long long t = lo; t < m && cs[t] <= k && ok; ++t)
+                    if (cl[t] == best) ok = idx < o1 && F[idx++] == cs[t];
+            ok = ok && idx == o1;
+        }
+        if (k == 1) ok = ok && O[0] == 0 && O[1] == 0 && L[0] == 0;
+        if (k == n) ok = ok && O[n + 1] == T;
+    }
+    if (ls) {
+        ok = ok && ls[k] == first && ll[k] == best;
+        if (k == 1) ok = ok && ls[0] == -1 && ll[0] == 0;
+    }
+    if (!ok) atomicAdd(bad, 1ull);
+}
+
 }  // namespace
+
+long long check_answers(rs_ctx *c, const long long *d_cs, const long long *d_cl, long long m, long long n,
+                        const long long *d_L, const long long *d_O, const long long *d_F, long long T,
+                        const long long *d_ls, const long long *d_ll) {
+    if (n <= 0) return 0;
+    unsigned long long *bad = (unsigned long long *)((char *)buf(c, B_SMALL, 4096) + 256);
+    RS_CUDA(cudaMemsetAsync(bad, 0, sizeof(*bad), c->stream));
+    RS_LAUNCH(c, k_check_answers, grid_for(n, 256), 256, 0, d_cs, d_cl, m, n, d_L, d_O, d_F, T, d_ls, d_ll,
+              bad);
+    unsigned long long h = 0;
+    fetch_small(c, &h, bad, sizeof(h));
+    return (long long)h;
+}
 
 bool verify_structures(rs_ctx *c, const unsigned char *d_text, long long n, const long long *d_sa,
                        const long long *d_rank, const long long *d_lcp) {

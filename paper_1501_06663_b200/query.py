@@ -11,6 +11,7 @@ they answer one k and have no data-parallel work to offload.
 
 from __future__ import annotations
 
+import ctypes
 from bisect import bisect_left
 from dataclasses import dataclass, field
 from typing import NamedTuple
@@ -262,3 +263,26 @@ def all_positions(
                 raise ValueError("structures arrays have inconsistent sizes")
             ctx.call("rs_set_structures", None, _native.i64(rank), _native.i64(lcp), n)
         return _run(ctx, mode, path, n, pinned)
+
+
+def count_wrong_answers(c: CompactLlr, n: int, all_answers: AllAnswers | None = None,
+                        leftmost: LeftmostAnswers | None = None) -> int:
+    """Number of positions whose answers disagree with the compact entries
+    ``c`` under the reference's Algorithm 4 as written (binary search of the
+    first covering entry + forward walk, ``_kernels_numba.py:74-85, 158-195``),
+    checked on device by a kernel that shares no code with the scan kernels.
+    Not part of the reference API: a parity property for large inputs."""
+    ctx = _native.context()
+    starts = np.ascontiguousarray(c.starts, dtype=np.int64)
+    lengths = np.ascontiguousarray(c.lengths, dtype=np.int64)
+    bad = np.zeros(1, np.int64)
+    null = ctypes.POINTER(ctypes.c_int64)()
+    a = (null, null, null, 0) if all_answers is None else (
+        _native.i64(all_answers.lengths), _native.i64(all_answers.offsets),
+        _native.i64(all_answers.flat_starts), int(all_answers.flat_starts.size))
+    lm = (null, null) if leftmost is None else (_native.i64(leftmost.starts),
+                                               _native.i64(leftmost.lengths))
+    with ctx.lock:
+        ctx.call("rs_check_answers", _native.i64(starts), _native.i64(lengths), int(starts.size),
+                 int(n), *a, *lm, _native.i64(bad))
+    return int(bad[0])

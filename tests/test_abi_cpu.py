@@ -103,3 +103,34 @@ def test_workload_generators_shapes():
     assert f.size == 100_000
     p = workloads.planted_dna(100_000, 2)
     assert p.size == 100_000
+
+
+def test_bruteforce_api_matches_reference_golden():
+    """is_repeat / oracle_llr / oracle_all_lr (reference oracle.py, exported by
+    __init__.py:20) against the reference's own answers for small golden cases."""
+    import paper_1501_06663_b200 as rb
+    from conftest import golden_cases
+    from paper_1501_06663_b200.bruteforce import oracle_all_positions
+    checked = 0
+    for c in golden_cases():
+        if not 1 <= c.n <= 40:
+            continue
+        t = rb.Text(c.data)
+        for k in range(1, c.n + 1):
+            lo, hi = int(c.a_offsets[k]), int(c.a_offsets[k + 1])
+            want = [(int(s), int(c.a_lengths[k])) for s in c.a_flat[lo:hi]]
+            assert [tuple(a) for a in rb.oracle_all_lr(t, k)] == want
+            r = rb.oracle_llr(t, k)
+            assert (r.start, r.length) == ((k, int(c.raw[k])) if c.raw[k] else (-1, 0))
+        assert [tuple(a) for a in oracle_all_positions(t, "leftmost")] == \
+            list(zip(c.l_starts[1:].tolist(), c.l_lengths[1:].tolist()))
+        checked += 1
+    assert checked > 300
+    t = rb.Text.from_str("abcabcddbca")  # test_query.py:61-63
+    assert rb.is_repeat(t, 1, 3) and not rb.is_repeat(t, 1, 4)
+    with pytest.raises(IndexError):
+        rb.is_repeat(t, 0, 1)
+    with pytest.raises(IndexError):
+        rb.oracle_llr(t, 12)
+    with pytest.raises(IndexError):
+        rb.oracle_all_lr(t, 0)

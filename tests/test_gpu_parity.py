@@ -275,6 +275,28 @@ def test_parallel_scan_gpu(rng):
         assert np.array_equal(rb.parallel_scan(v, rb.ExecPolicy.parallel(4)), np.cumsum(v))
 
 
+def test_parallel_scan_full_int64(rng):
+    """engine.py:77-110 is np.cumsum over any int64: negative values, prefixes
+    beyond 2^62 and two's-complement wraparound, over many look-back tiles."""
+    big = np.iinfo(np.int64).max
+    cases = [np.full(3000, -1, np.int64), np.full(50000, -7, np.int64),
+             np.full(10000, 1 << 61, np.int64), np.full(10000, -(1 << 61), np.int64),
+             np.full(5000, big, np.int64), np.full(5000, big // 3, np.int64),
+             np.array([big, 1, big, 1, -big, -5], np.int64)]
+    for n in (2047, 2048, 2049, 1 << 20, (1 << 22) + 12345):
+        cases.append(rng.integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64))
+        cases.append(rng.integers(np.iinfo(np.int64).min, big, size=n, dtype=np.int64,
+                                  endpoint=True))
+    for v in cases:
+        with np.errstate(over="ignore"):
+            want = np.cumsum(v)
+        assert np.array_equal(rb.parallel_scan(v, rb.ExecPolicy.parallel(4)), want)
+    flags = np.zeros(1 << 21, np.int64)
+    flags[1:] = rng.integers(-3, 1 << 40, size=flags.size - 1)
+    ps = rb.prefix_sum(flags)
+    assert ps[0] == 0 and np.array_equal(ps[1:], np.cumsum(flags[1:]))
+
+
 def test_kernels_launch_from_native_library():
     from paper_1501_06663_b200 import _native
     ctx = _native.context()

@@ -128,3 +128,37 @@ def test_oracle_walk_stats_match_reference_golden():
     for c in golden_cases():
         assert np.array_equal(oracle.walk_steps_raw(c.raw), c.w_raw), c
         assert np.array_equal(oracle.walk_steps_compact(c.c_starts, c.c_lengths, c.n), c.w_comp), c
+
+
+@pytest.mark.parametrize("name", ["acgt_1e6_seed99", "C2_shape_2p21", "C4_shape_2p21",
+                                  "C5_shape_2p20", "periodic_2p20"])
+def test_oracle32_matches_reference_digests(name):
+    """oracle/oracle32.c (the u32 restatement that produced the committed 1 GiB
+    C5 digests, tests/golden/make_fullsize.py) reproduces every reference
+    digest, m, T and max LLR of the 1-2 Mi reference digest set."""
+    from paper_1501_06663_b200 import workloads  # noqa: F401  (used by eval)
+    rec = golden_digests()[name]
+    got = oracle.digests32(eval(rec["expr"]), chunk=1 << 18)
+    for key, val in got.items():
+        if key in rec:
+            assert val == rec[key], (name, key)
+    assert {"sa", "lcp", "raw", "c_starts", "l_starts", "a_offsets", "a_flat", "T"} <= set(got)
+
+
+def test_oracle32_matches_oracle_small(rng):
+    """Same digests as the int64 oracle on small arbitrary-byte inputs."""
+    for _ in range(30):
+        n = int(rng.integers(1, 3000))
+        sigma = int(rng.integers(1, 257))
+        alpha = rng.choice(256, size=sigma, replace=False).astype(np.uint8)
+        data = rng.choice(alpha, size=n)
+        got = oracle.digests32(data, chunk=int(rng.integers(1, 600)))
+        sa, rank, lcp = oracle.build_suffix_structures(data)
+        raw = oracle.build_raw_llr(rank, lcp, 0)
+        s, l = oracle.build_compact_llr(raw, 0)
+        al, ao, af = oracle.all_all_positions(n, "compact", raw, (s, l), 0)
+        st, ln = oracle.leftmost_all_positions(n, "compact", raw, (s, l), 0)
+        want = {"sa": sa, "rank": rank, "lcp": lcp, "raw": raw, "c_starts": s, "c_lengths": l,
+                "a_lengths": al, "a_offsets": ao, "a_flat": af, "l_starts": st, "l_lengths": ln}
+        for key, arr in want.items():
+            assert got[key] == digest(arr), (n, key)
