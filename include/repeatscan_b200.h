@@ -152,6 +152,10 @@ int rs_get_compact(rs_ctx *ctx, int64_t *starts, int64_t *lengths);
 int rs_reset(rs_ctx *ctx);
 /* Drop everything derived from the loaded text (keeps the text resident). */
 int rs_clear_derived(rs_ctx *ctx);
+/* Drop the raw LLR / compact entries but keep the suffix structures on
+ * device: the next rs_query recomputes llr.py:63-123 from them, like the
+ * reference's all_positions(text, structures=s) (query.py:234-239). */
+int rs_clear_llr(rs_ctx *ctx);
 /* Per-kernel profiling: while enabled every launch is bracketed by CUDA
  * events on the context stream and tagged with its algorithmic HBM bytes.
  * rs_profile_end aggregates per kernel name; read them with rs_profile_kernel. */

@@ -53,6 +53,7 @@ def _load():
     sig = {
         "or_suffix_array_0based": (c_int, [_U8P, i64, _I64P]),
         "or_build_structures": (c_int, [_U8P, i64, _I64P, _I64P, _I64P]),
+        "or_build_structures_par": (c_int, [_U8P, i64, _I64P, _I64P, _I64P, c_int]),
         "or_kasai_lcp": (None, [_U8P, _I64P, _I64P, _I64P, i64]),
         "or_fill_raw_llr": (None, [i64, i64, _I64P, _I64P, _I64P]),
         "or_fill_flags": (None, [i64, i64, _I64P, _I64P]),
@@ -95,14 +96,23 @@ def _workers(workers: int | None) -> int:
 
 
 # -- suffixes.py:56-66 --------------------------------------------------------
-def build_suffix_structures(data: np.ndarray):
-    """(sa, rank, lcp) int64 1-based padded, as ``build_suffix_structures``."""
+def build_suffix_structures(data: np.ndarray, workers: int = 1):
+    """(sa, rank, lcp) int64 1-based padded, as ``build_suffix_structures``.
+
+    workers == 1: the line-by-line restatement (suffixes.py:31-66).
+    workers > 1: the threaded variant (or_build_structures_par: radix-sorted
+    prefix doubling + chunked Kasai, identical output) used to give the CPU
+    baseline its ``structures=`` input at full size."""
     data = np.ascontiguousarray(data, dtype=np.uint8)
     n = int(data.size)
     sa = np.zeros(n + 1, np.int64)
     rank = np.zeros(n + 1, np.int64)
     lcp = np.zeros(n + 2, np.int64)
-    if n:
+    if n and workers > 1:
+        rc = _load().or_build_structures_par(_u8(data), n, _p(sa), _p(rank), _p(lcp), int(workers))
+        if rc != 0:
+            raise MemoryError("oracle suffix sort out of memory")
+    elif n:
         rc = _load().or_build_structures(_u8(data), n, _p(sa), _p(rank), _p(lcp))
         if rc != 0:
             raise MemoryError("oracle suffix sort out of memory")

@@ -408,3 +408,159 @@ int or_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------ */
+/* Threaded build_suffix_structures (same output as or_build_structures).    */
+/* Used only to give the CPU baseline / reference arm of bench.py its        */
+/* `structures=` input at 256 Mi in seconds instead of minutes (the query    */
+/* path the arm times starts from given structures, query.py:234).  Same     */
+/* prefix doubling as suffixes.py:31-53 -- per round sort by (rank[i],       */
+/* rank[i+k] or -1), dense re-rank, double k until ranks are distinct --    */
+/* with the sort done as a parallel LSD radix sort of packed 64-bit keys    */
+/* (the SA is unique, so any correct sort yields the reference's SA), then  */
+/* rank inversion and Kasai's LCP (_kernels_numba.py:15-30) over T chunks   */
+/* of text positions, each restarting h at 0 (h is only a lower bound).     */
+/* ------------------------------------------------------------------------ */
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+static int bits_for(u64 x) { int b = 0; while (b < 64 && (x >> b)) ++b; return b; }
+
+int or_build_structures_par(const uint8_t *data, i64 n, i64 *sa, i64 *rank_out, i64 *lcp, int workers) {
+    if (n <= 0) return 0;
+    if (n >= (1ll << 32) - 2) return -2;
+    int T = clamp_parts(workers, n);
+    u64 *keyA = (u64 *)malloc(sizeof(u64) * (size_t)n), *keyB = (u64 *)malloc(sizeof(u64) * (size_t)n);
+    u32 *valA = (u32 *)malloc(sizeof(u32) * (size_t)n), *valB = (u32 *)malloc(sizeof(u32) * (size_t)n);
+    u32 *rank = (u32 *)malloc(sizeof(u32) * (size_t)n);
+    i64 *cnt = (i64 *)malloc(sizeof(i64) * (size_t)(T + 1));
+    if (!keyA || !keyB || !valA || !valB || !rank || !cnt) {
+        free(keyA); free(keyB); free(valA); free(valB); free(rank); free(cnt);
+        return -1;
+    }
+#pragma omp parallel for num_threads(T) schedule(static)
+    for (i64 i = 0; i < n; ++i) rank[i] = data[i]; /* order-equivalent to :34-38 */
+    u32 maxrank = 255;
+    for (i64 k = 1;; k *= 2) {
+        int rb = bits_for((u64)maxrank + 1);
+#pragma omp parallel for num_threads(T) schedule(static)
+        for (i64 i = 0; i < n; ++i) {
+            u64 k2 = (i + k < n) ? (u64)rank[i + k] + 1 : 0; /* -1 past the end -> 0 */
+            keyA[i] = ((u64)rank[i] << rb) | k2;
+            valA[i] = (u32)i;
+        }
+        /* radix sort in place (ping-pong tracked locally) */
+        {
+            u64 *kin = keyA, *kout = keyB;
+            u32 *vin = valA, *vout = valB;
+            const int DB = 11, NB = 1 << DB;
+            int bits = 2 * rb + 1;
+            i64 *hist = (i64 *)calloc((size_t)T * NB, sizeof(i64));
+            for (int shift = 0; shift < bits; shift += DB) {
+                memset(hist, 0, sizeof(i64) * (size_t)T * NB);
+#pragma omp parallel num_threads(T)
+                {
+                    int t = 0;
+#ifdef _OPENMP
+                    t = omp_get_thread_num();
+#endif
+                    i64 a, b;
+                    chunk_bounds(0, n, T, t, &a, &b);
+                    i64 *h = hist + (size_t)t * NB;
+                    for (i64 i = a; i < b; ++i) h[(kin[i] >> shift) & (NB - 1)]++;
+                }
+                int distinct = 0;
+                for (int d = 0; d < NB && distinct < 2; ++d) {
+                    i64 s = 0;
+                    for (int t = 0; t < T; ++t) s += hist[(size_t)t * NB + d];
+                    distinct += s > 0;
+                }
+                if (distinct < 2) continue;
+                i64 run = 0;
+                for (int d = 0; d < NB; ++d)
+                    for (int t = 0; t < T; ++t) {
+                        i64 c = hist[(size_t)t * NB + d];
+                        hist[(size_t)t * NB + d] = run;
+                        run += c;
+                    }
+#pragma omp parallel num_threads(T)
+                {
+                    int t = 0;
+#ifdef _OPENMP
+                    t = omp_get_thread_num();
+#endif
+                    i64 a, b;
+                    chunk_bounds(0, n, T, t, &a, &b);
+                    i64 *h = hist + (size_t)t * NB;
+                    for (i64 i = a; i < b; ++i) {
+                        i64 p = h[(kin[i] >> shift) & (NB - 1)]++;
+                        kout[p] = kin[i];
+                        vout[p] = vin[i];
+                    }
+                }
+                u64 *tk = kin; kin = kout; kout = tk;
+                u32 *tv = vin; vin = vout; vout = tv;
+            }
+            free(hist);
+            if (kin != keyA) { /* result lives in the B buffers: swap roles */
+                u64 *tk = keyA; keyA = keyB; keyB = tk;
+                u32 *tv = valA; valA = valB; valB = tv;
+            }
+        }
+        /* :44-51 dense re-rank by key changes (parallel count + carry) */
+#pragma omp parallel num_threads(T)
+        {
+            int t = 0;
+#ifdef _OPENMP
+            t = omp_get_thread_num();
+#endif
+            i64 a, b, c = 0;
+            chunk_bounds(0, n, T, t, &a, &b);
+            for (i64 j = (a == 0 ? 1 : a); j < b; ++j) c += keyA[j] != keyA[j - 1];
+            cnt[t + 1] = c;
+        }
+        cnt[0] = 0;
+        for (int t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+#pragma omp parallel num_threads(T)
+        {
+            int t = 0;
+#ifdef _OPENMP
+            t = omp_get_thread_num();
+#endif
+            i64 a, b, r;
+            chunk_bounds(0, n, T, t, &a, &b);
+            r = cnt[t];
+            for (i64 j = a; j < b; ++j) {
+                if (j > 0 && keyA[j] != keyA[j - 1]) ++r;
+                rank[valA[j]] = (u32)r;
+            }
+        }
+        maxrank = (u32)cnt[T];
+        if ((i64)maxrank == n - 1) break; /* :40 all ranks distinct */
+    }
+#pragma omp parallel for num_threads(T) schedule(static)
+    for (i64 j = 0; j < n; ++j) {
+        sa[j + 1] = (i64)valA[j] + 1;        /* :63 */
+        rank_out[valA[j] + 1] = j + 1;       /* :64 */
+    }
+    free(keyA); free(keyB); free(valA); free(valB); free(rank); free(cnt);
+    /* :65 kasai_lcp over T chunks of text positions */
+#pragma omp parallel num_threads(T)
+    {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        i64 a, b, h = 0;
+        chunk_bounds(1, n + 1, T, t, &a, &b);
+        for (i64 i = a; i < b; ++i) {
+            i64 r = rank_out[i];
+            if (r == 1) { h = 0; continue; }
+            i64 j = sa[r - 1];
+            while (i + h <= n && j + h <= n && data[i + h - 1] == data[j + h - 1]) ++h;
+            lcp[r] = h;
+            if (h > 0) --h;
+        }
+    }
+    return 0;
+}

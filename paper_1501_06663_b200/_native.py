@@ -68,6 +68,7 @@ SIGNATURES = {
     "rs_get_compact": [_CTX, _I64P, _I64P],
     "rs_reset": [_CTX],
     "rs_clear_derived": [_CTX],
+    "rs_clear_llr": [_CTX],
     "rs_profile_begin": [_CTX],
     "rs_profile_end": [_CTX, ctypes.POINTER(ctypes.c_int)],
     "rs_profile_kernel": [_CTX, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, _I64P,

@@ -769,6 +769,15 @@ int rs_clear_derived(rs_ctx *c) {
     });
 }
 
+int rs_clear_llr(rs_ctx *c) {
+    return guarded(c, [&] {
+        if (!c->have_lcp) fail(RS_ESTATE, "no structures on device");
+        c->have_raw = c->have_compact = false;
+        c->raw_from_round0 = false;
+        c->out_mode = -1;
+    });
+}
+
 int rs_profile_begin(rs_ctx *c) {
     return guarded(c, [&] {
         c->prof.clear();

@@ -162,3 +162,18 @@ def test_oracle32_matches_oracle_small(rng):
                 "a_lengths": al, "a_offsets": ao, "a_flat": af, "l_starts": st, "l_lengths": ln}
         for key, arr in want.items():
             assert got[key] == digest(arr), (n, key)
+
+
+@pytest.mark.parametrize("workers", [3, 8])
+def test_threaded_structures_match_reference(workers):
+    """or_build_structures_par (the CPU baseline's structures= builder) gives the
+    reference's arrays: golden cases and the 1 Mi reference digests."""
+    from paper_1501_06663_b200 import workloads  # noqa: F401  (used by eval)
+    for c in golden_cases():
+        sa, rank, lcp = oracle.build_suffix_structures(c.data, workers=workers)
+        assert np.array_equal(sa, c.sa) and np.array_equal(rank, c.rank), c
+        assert np.array_equal(lcp, c.lcp), c
+    for name in ("C1_2p20", "C5_shape_2p20"):
+        rec = golden_digests()[name]
+        sa, rank, lcp = oracle.build_suffix_structures(eval(rec["expr"]), workers=workers)
+        assert (digest(sa), digest(rank), digest(lcp)) == (rec["sa"], rec["rank"], rec["lcp"])
