@@ -1,24 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: positions/sec of the all-longest-repeat query (BASELINE.json metric).
 
-Workload (N=1): config C3 -- 256 MiB i.i.d. ACGT (seed 3), END TO END on the
-device: suffix sort -> rank -> LCP -> raw LLR -> compaction -> all-ties scan,
-results written in the reference int64 CSR layout.  One step = one full pass
-over the text; the text (256 MiB > 126 MB L2) stays resident in HBM, every
-derived array is rebuilt each step.
+Workload (N=1): config C3 -- 256 MiB i.i.d. ACGT (seed 3), all ties, compact
+path.  Like for like with the reference arm: one step
+is the reference's query path from GIVEN suffix structures (query.py:234):
+raw LLR (llr.py:63-72) -> compaction (llr.py:119-123) -> all-ties scan with
+the int64 CSR answers written (query.py:187-215).  The structures are built
+once, untimed, on the device and passed back in as the reference's int64
+SuffixStructures; every step rebuilds raw LLR, compaction and answers from
+them (256 MiB text and 2 GiB of structures > 126 MB L2).
 
-  value  : n * steps / device time of the K timed steps (CUDA events on the
-           library stream), positions/s.
-  e2e    : the same metric through the public API a user calls,
-           ``all_positions(Text, mode="all", path="compact")``: H2D of the text
-           from pinned host memory + the whole device path + D2H of lengths,
-           offsets and tie starts (int64) into pinned host arrays.
-  roofline: dominant kernel of the step, algorithmic bytes / its average
-           launch time (per-kernel CUDA events inside the timed region).
-  cpu_baseline: the CPU oracle port (oracle/, C + OpenMP, restating the
-           reference algorithm) on a bounded prefix of the same workload.
+  value     : n * steps / device time of the K timed steps (CUDA events on
+              the library stream), positions/s.
+  e2e       : the public call a user makes, ``all_positions(Text, mode="all",
+              path="compact")`` with host buffers: text H2D, suffix sort, LCP,
+              query, D2H of the int64 lengths/offsets/tie starts into numpy.
+  e2e_structures_given: the reference arm's exact call (structures= given).
+  end_to_end_device: SA + LCP + query from the resident text (device only).
+  parity    : digests of the answers vs tests/golden/fullsize_digests.json.
+  roofline  : dominant kernel of the step, algorithmic bytes / its average
+              launch time (per-kernel CUDA events, separate instrumented pass).
+  cpu_baseline: one full-size step of the CPU oracle port (oracle/, C +
+              OpenMP restating the reference) from the same structures.
 
-``--impl reference`` times that CPU port alone as the reference arm.
+``--impl reference`` times that CPU port as the reference arm on the same
+config (structures built untimed by the oracle's threaded prefix doubling).
 Multi-GPU (torchrun, N>1): see paper_1501_06663_b200/distributed.py.
 """
 
@@ -115,37 +121,37 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-# CPU baseline / reference arm: the oracle port (C + OpenMP) on a bounded prefix
+# CPU baseline / reference arm: the oracle port (C + OpenMP) of the reference's query
+# path on the SAME workload, structures given
 # ---------------------------------------------------------------------------------------
-def cpu_run(data: np.ndarray, threads: int) -> dict:
-    """SA+LCP (single thread, as the reference's numpy suffixes.py:31-66) + raw LLR +
-    compaction + all-ties compact query (threaded like ExecPolicy.parallel)."""
+def cpu_query_step(n: int, rank: np.ndarray, lcp: np.ndarray, threads: int) -> dict:
+    """One reference query pass from given structures (query.py:234-239 with
+    ``structures=`` supplied): build_raw_llr (llr.py:63-72) -> build_compact_llr
+    (llr.py:119-123) -> _all_all_positions on the compact path (query.py:187-215),
+    each stage split over ``threads`` like ExecPolicy.parallel(threads)."""
     import oracle
     t0 = time.perf_counter()
-    sa, rank, lcp = oracle.build_suffix_structures(data)
-    t1 = time.perf_counter()
     raw = oracle.build_raw_llr(rank, lcp, threads)
+    t1 = time.perf_counter()
     c = oracle.build_compact_llr(raw, threads)
     t2 = time.perf_counter()
-    lengths, offsets, flat = oracle.all_all_positions(data.size, "compact", raw, c, threads)
+    lengths, offsets, flat = oracle.all_all_positions(n, "compact", raw, c, threads)
     t3 = time.perf_counter()
-    return {"n": int(data.size), "build_s": t1 - t0, "llr_compact_s": t2 - t1, "query_s": t3 - t2,
-            "total_s": t3 - t0, "T": int(flat.size)}
+    return {"raw_llr_s": t1 - t0, "compaction_s": t2 - t1, "query_s": t3 - t2, "total_s": t3 - t0,
+            "T": int(flat.size), "m": int(c[0].size)}
 
 
-def cpu_baseline(config: str, sample_n: int, threads: int) -> dict:
-    from paper_1501_06663_b200 import workloads
-    data = workloads.make(config, sample_n)
-    r = cpu_run(data, threads)
-    return {"value": r["n"] / r["total_s"], "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"{config} generator at n={r['n']} (bounded prefix of the workload): "
-                       f"SA+LCP {r['build_s']:.2f}s (1 thread, like the reference numpy build), "
-                       f"LLR+compaction {r['llr_compact_s']:.3f}s + all-ties query {r['query_s']:.3f}s "
-                       f"({threads} threads)"),
-            "query_only_value": r["n"] / (r["llr_compact_s"] + r["query_s"])}
+def cpu_structures(data: np.ndarray, threads: int):
+    """CPU suffix structures for the baseline's ``structures=`` input (untimed):
+    the oracle's threaded prefix doubling, identical to the reference's arrays."""
+    import oracle
+    return oracle.build_suffix_structures(data, workers=threads)
 
 
 def run_reference(args) -> None:
+    """Reference arm: the reference CPU path (oracle port) on our arm's config,
+    metric and unit: n / (raw LLR + compaction + all-ties query) with the
+    suffix structures given, every stage on all host threads."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -153,25 +159,31 @@ def run_reference(args) -> None:
     import oracle
     oracle.build() if not (REPO / "oracle" / "liboracle.so").exists() else None
     threads = os.cpu_count() or 1
-    n = args.ref_sample
-    data = workloads.make(args.config, n)
+    data = workloads.make(args.config, args.n)
+    n = int(data.size)
+    t0 = time.perf_counter()
+    _, rk, lc = cpu_structures(data, threads)
+    build_s = time.perf_counter() - t0
     for _ in range(args.warmup):
-        cpu_run(data, threads)
-    times = []
-    for _ in range(args.steps):
-        times.append(cpu_run(data, threads)["total_s"])
-    t = float(np.sum(times))
+        cpu_query_step(n, rk, lc, threads)
+    steps = [cpu_query_step(n, rk, lc, threads) for _ in range(args.steps)]
+    t = float(sum(r["total_s"] for r in steps))
     value = n * args.steps / t
+    stage = {k: float(np.mean([r[k] for r in steps])) for k in ("raw_llr_s", "compaction_s", "query_s")}
+    sample = (f"{args.config} at full size n={n}: each step = raw LLR + compaction + all-ties compact "
+              f"query from given structures (oracle/repeatscan_oracle.c restating llr.py / query.py / "
+              f"_kernels_numba.py, {threads} threads like ExecPolicy.parallel); structures built untimed "
+              f"in {build_s:.1f} s by the oracle's threaded prefix doubling")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8 text / int64 answers", "data": "synthetic",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
-                   "note": "bounded prefix of the workload per step; CPU port of the reference"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.config} generator prefix n={n} per step, SA 1 thread, "
-                                   f"query stages {threads} threads (oracle/repeatscan_oracle.c)"},
+                   "timed": "raw LLR + compaction + all-ties query, structures given (query.py:234)",
+                   "T": steps[0]["T"], "m": steps[0]["m"]},
+        "stages_s": stage,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -220,106 +232,168 @@ def roofline_of(profile: list[dict], steps: int) -> tuple[dict, list[dict]]:
     return roof, rows
 
 
+def _digest(a: np.ndarray) -> str:
+    import hashlib
+    return hashlib.sha256(memoryview(np.ascontiguousarray(a, dtype=np.int64)).cast("B")).hexdigest()[:16]
+
+
+def parity_of(config: str, n: int, res) -> dict:
+    """Compare the answers the bench produced with the committed full-size
+    digests (tests/golden/fullsize_digests.json: reference / pinned oracle)."""
+    path = REPO / "tests" / "golden" / "fullsize_digests.json"
+    try:
+        rec = json.loads(path.read_text()).get(config)
+    except (OSError, ValueError):
+        rec = None
+    if rec is None or rec.get("n") != n:
+        return {"checked": False, "why": f"no committed digests for {config} at n={n}"}
+    got = {"a_lengths": _digest(res.lengths), "a_offsets": _digest(res.offsets),
+           "a_flat": _digest(res.flat_starts)}
+    ok = all(rec[k] == v for k, v in got.items()) and rec["T"] == int(res.flat_starts.size)
+    return {"checked": True, "bit_exact": bool(ok), "source": rec.get("source"),
+            "arrays": "all-ties lengths, offsets, flat tie starts (sha256 of the int64 arrays)"}
+
+
 def run_single(args) -> None:
-    from paper_1501_06663_b200 import Text, _native, all_positions, workloads
+    from paper_1501_06663_b200 import SuffixStructures, Text, _native, all_positions, workloads
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     ctx = _native.context(dev)
-    t_gen = time.perf_counter()
     data = workloads.make(args.config, args.n)
     n = int(data.size)
-    t_gen = time.perf_counter() - t_gen
     host_text = _native.pinned_pool.empty(n, np.uint8)
     host_text[:] = data
+    total = np.zeros(1, np.int64)
 
-    # ---- device-resident steps ----
     with ctx.lock:
+        # ---- structures (untimed, like the reference arm): built on device,
+        # handed back to the host as the reference's int64 SuffixStructures ----
+        sa = np.empty(n + 1, np.int64)
+        rk = np.empty(n + 1, np.int64)
+        lc = np.empty(n + 2, np.int64)
         ctx.call("rs_set_text", _native.u8(host_text), n)
-        total = np.zeros(1, np.int64)
+        ctx.call("rs_build_structures")
+        ctx.call("rs_get_structures", _native.i64(sa), _native.i64(rk), _native.i64(lc))
+        ctx.call("rs_set_structures", None, _native.i64(rk), _native.i64(lc), n)
 
-        def step():
-            ctx.call("rs_clear_derived")
+        def q_step():  # llr.py:63-123 + query.py:187-215 from resident structures
+            ctx.call("rs_clear_llr")
             ctx.call("rs_query", 1, 1, _native.i64(total))
 
         clocks = ClockSampler(dev)
         clocks.start()  # sampling spans warm-up + timed steps (nvidia-smi needs ~0.5 s to start)
         for _ in range(args.warmup):
-            step()
+            q_step()
         ctx.synchronize()
         launches0 = ctx.launches()
-        ctx.profile_begin()
         ctx.record(0)
         for _ in range(args.steps):
-            step()
+            q_step()
         ctx.record(1)
-        dev_ms = ctx.elapsed_ms(0, 1)
-        profile = ctx.profile_end()
+        q_ms = ctx.elapsed_ms(0, 1) / args.steps
         launches = ctx.launches() - launches0
-        stages = ctx.stage_times()
-        rounds = ctx.sa_rounds()
         T = int(total[0])
-        # un-instrumented timing of the same steps (profiling events add a little overhead)
+        # per-kernel breakdown: a separate instrumented pass (events around every launch)
+        ctx.profile_begin()
+        for _ in range(args.steps):
+            q_step()
+        ctx.synchronize()
+        profile = ctx.profile_end()
+        q_stages = ctx.stage_times()
+        clk = clocks.stop()
+
+        # ---- the whole device path from the resident text (SA-inclusive, extra key) ----
+        ctx.call("rs_set_text", _native.u8(host_text), n)
+
+        def full_step():
+            ctx.call("rs_clear_derived")
+            ctx.call("rs_query", 1, 1, _native.i64(total))
+
+        for _ in range(args.warmup):
+            full_step()
         ctx.synchronize()
         ctx.record(0)
         for _ in range(args.steps):
-            step()
+            full_step()
         ctx.record(1)
-        dev_ms_plain = ctx.elapsed_ms(0, 1)
-        clk = clocks.stop()
-    ms_per_step = min(dev_ms, dev_ms_plain) / args.steps
-    value = n / (ms_per_step * 1e-3)
+        full_ms = ctx.elapsed_ms(0, 1) / args.steps
+        full_stages = ctx.stage_times()
+        rounds = ctx.sa_rounds()
+        assert int(total[0]) == T
 
-    # ---- e2e through the public API (pinned host in/out) ----
+    value = n / (q_ms * 1e-3)
+
+    # ---- e2e through the public API with host buffers (default call) ----
     t = Text(host_text)
-    e2e_ms = []
-    res = None
-    for i in range(args.warmup + args.steps):
-        del res
-        res = None
-        ctx.synchronize()
-        ctx.record(2)
-        res = all_positions(t, mode="all", path="compact", pinned=True)
-        ctx.record(3)
-        if i >= args.warmup:
-            e2e_ms.append(ctx.elapsed_ms(2, 3))
-    e2e_T = int(res.flat_starts.size)
-    h2d = n
-    d2h = 8 * (n + 1) + 8 * (n + 2) + 8 * e2e_T
-    e2e_val = n / (np.mean(e2e_ms) * 1e-3)
-    assert e2e_T == T, (e2e_T, T)
+    s_host = SuffixStructures(sa=sa, rank=rk, lcp=lc)
+
+    def e2e_run(fn, reps):
+        out, res = [], None
+        for i in range(args.warmup + reps):
+            res = None
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            res = fn()
+            out.append(time.perf_counter() - t0)
+        return float(np.mean(out[args.warmup:])), res
+
+    e2e_s, res = e2e_run(lambda: all_positions(t, mode="all", path="compact"), args.steps)
+    parity = parity_of(args.config, n, res)
+    assert int(res.flat_starts.size) == T
+    del res
+    e2e_struct_s, res = e2e_run(
+        lambda: all_positions(t, mode="all", path="compact", structures=s_host), max(3, args.steps // 3))
+    assert int(res.flat_starts.size) == T
+    del res
+    d2h = 8 * (n + 1) + 8 * (n + 2) + 8 * T
 
     roof, rows = roofline_of(profile, args.steps)
     scan = next((r for r in rows if r["kernel"].startswith("k_query")), None)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
+        "warmup": args.warmup, "ms_per_step": q_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32 device indices / int64 answers",
         "data": "synthetic",
         "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
-                   "pipeline": "SA (prefix doubling: onesweep LSD radix, small tied groups sorted "
-                               "directly) + LCP (round-0 keys + direct comparison; Kasai for "
-                               "repetitive text) + raw LLR + compaction fused into the all-ties "
-                               "scan (TMA-staged)",
-                   "parallelism": "single GPU", "l2": "input 256 MiB > 126 MB L2; all arrays "
-                                                     "rebuilt each step",
-                   "T": T, "sa_rounds": rounds},
-        "gpu_launches": launches // 1,
+                   "timed": "raw LLR + compaction + all-ties query with the suffix structures given "
+                            "(query.py:234; BASELINE.md section 2), int64 CSR answers written on device",
+                   "structures": "built untimed on device, passed back in as the reference's int64 "
+                                 "SuffixStructures (rank, lcp)",
+                   "parallelism": "single GPU",
+                   "l2": "input 256 MiB > 126 MB L2; raw LLR, compaction and answers rebuilt each step",
+                   "T": T},
+        "gpu_launches": launches,
         "clocks": clk,
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": float(np.mean(e2e_ms)),
-                "path": "all_positions(Text, mode='all', path='compact', pinned=True)"},
+        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n, "d2h_bytes_per_step": d2h,
+                "ms_per_step": 1e3 * e2e_s,
+                "path": "all_positions(Text, mode='all', path='compact') -- default call, host text in, "
+                        "int64 numpy answers out (suffix sort + LCP + query on device, inside the timing)"},
+        "e2e_structures_given": {
+            "value": n / e2e_struct_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_struct_s,
+            "h2d_bytes_per_step": 16 * (n + 1) + 8, "d2h_bytes_per_step": d2h,
+            "path": "all_positions(Text, mode='all', path='compact', structures=SuffixStructures) -- "
+                    "the reference arm's exact call"},
+        "parity": parity,
         "roofline": roof,
         "scan_kernel": ({"kernel": scan["kernel"], "achieved": scan["achieved_gbs"], "frac": scan["frac"],
                          "ms_per_step": scan["ms_per_step"], "bytes_per_launch": scan["bytes_per_launch"],
                          "positions_per_s": n / (scan["avg_launch_ms"] * 1e-3)} if scan else None),
-        "stages_ms": stages,
+        "stages_ms": q_stages,
         "kernels": rows,
-        "query_only": {"value": n / (1e-3 * (stages["raw_llr"] + stages["compact"] + stages["query"])),
-                       "unit": UNIT, "what": "raw LLR + compaction + all-ties scan with SA/LCP resident"},
+        "end_to_end_device": {"value": n / (full_ms * 1e-3), "unit": UNIT, "ms_per_step": full_ms,
+                              "what": "suffix sort + LCP + raw LLR + compaction + all-ties query from the "
+                                      "resident text", "stages_ms": full_stages, "sa_rounds": rounds},
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_sample, os.cpu_count() or 1)
+        threads = os.cpu_count() or 1
+        cpu = cpu_query_step(n, rk, lc, threads)
+        line["cpu_baseline"] = {
+            "value": n / cpu["total_s"], "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"one step of the same workload at full size (n={n}, structures given): raw LLR "
+                       f"{cpu['raw_llr_s']:.2f}s + compaction {cpu['compaction_s']:.2f}s + all-ties query "
+                       f"{cpu['query_s']:.2f}s on {threads} threads (oracle/repeatscan_oracle.c)")}
+        assert cpu["T"] == T
     print(json.dumps(line), flush=True)
 
 
@@ -331,8 +405,6 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="C3")
     ap.add_argument("--n", type=int, default=None, help="override the config size")
-    ap.add_argument("--cpu-sample", type=int, default=8 << 20)
-    ap.add_argument("--ref-sample", type=int, default=4 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

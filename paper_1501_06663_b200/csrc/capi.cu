@@ -41,6 +41,12 @@ void dist_scan(rs_ctx *c, long long n, int mode, long long halo, long long *tota
 bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long count, const unsigned *d_raw,
                  long long kb, long long ke, int out_off, long long n_slots, long long min_lo = 1);
 
+void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind);
+bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long count, long long lo, long long hi,
+                    long long add);
+void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes);
+void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add);
+
 void fail(int code, const std::string &msg) { throw RsError{code, msg}; }
 
 void check_cuda(cudaError_t e, const char *what, const char *file, int line) {
@@ -304,6 +310,10 @@ int rs_destroy(rs_ctx *c) {
         if (c->events[i]) cudaEventDestroy(c->events[i]);
     for (auto e : c->prof_events) cudaEventDestroy(e);
     if (c->small_host) cudaFreeHost(c->small_host);
+    for (int i = 0; i < 2; ++i) {
+        if (c->xfer_host[i]) cudaFreeHost(c->xfer_host[i]);
+        if (c->xfer_ev[i]) cudaEventDestroy(c->xfer_ev[i]);
+    }
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return RS_OK;
@@ -510,7 +520,7 @@ int rs_set_text(rs_ctx *c, const uint8_t *text, int64_t n) {
             used[RS_STAGE_H2D] = true;
             unsigned char *d = (unsigned char *)buf(c, B_TEXT, (size_t)n + 128);
             RS_CUDA(cudaMemsetAsync(d + n, 0, 128, c->stream));
-            h2d(c, d, text, (size_t)n);
+            put_bytes(c, d, text, (size_t)n);
         }
         collect_stages(c, used);
         c->n = n;
@@ -525,20 +535,19 @@ int rs_set_structures(rs_ctx *c, const int64_t *sa, const int64_t *rank, const i
         bool keep_text = c->have_text && c->n == n;
         invalidate(c);
         c->have_text = keep_text;
-        long long *dtmp = (long long *)buf(c, B_I64A, 8 * (size_t)(n + 2));
         unsigned *disa = (unsigned *)buf(c, B_ISA, sizeof(unsigned) * (size_t)(n + 4));
         unsigned *dlcp = (unsigned *)buf(c, B_LCP, sizeof(unsigned) * (size_t)(n + 4));
         RS_CUDA(cudaMemsetAsync(dlcp, 0, sizeof(unsigned) * (size_t)(n + 4), c->stream));
-        if (n > 0) {
+        if (n > 0) {  // narrowed (range-checked) on the host, 4 bytes per value on the wire
             if (sa) {
                 unsigned *dsa = (unsigned *)buf(c, B_SA, sizeof(unsigned) * (size_t)(n + 4));
-                h2d(c, dtmp, sa + 1, 8 * (size_t)n);
-                narrow_i64_to_u32(c, dtmp, dsa, n, 1, n, -1, "sa");
+                if (!put_i64_as_u32(c, dsa, (const long long *)sa + 1, n, 1, n, -1))
+                    fail(RS_EINVAL, "sa has values out of range");
             }
-            h2d(c, dtmp, rank + 1, 8 * (size_t)n);
-            narrow_i64_to_u32(c, dtmp, disa, n, 1, n, -1, "rank");
-            h2d(c, dtmp, lcp + 1, 8 * (size_t)(n + 1));
-            narrow_i64_to_u32(c, dtmp, dlcp, n + 1, 0, n, 0, "lcp");
+            if (!put_i64_as_u32(c, disa, (const long long *)rank + 1, n, 1, n, -1))
+                fail(RS_EINVAL, "rank has values out of range");
+            if (!put_i64_as_u32(c, dlcp, (const long long *)lcp + 1, n + 1, 0, n, 0))
+                fail(RS_EINVAL, "lcp has values out of range");
         }
         RS_CUDA(cudaStreamSynchronize(c->stream));
         c->n = n;
@@ -623,18 +632,11 @@ int rs_get_structures(rs_ctx *c, int64_t *sa, int64_t *rank, int64_t *lcp) {
     return guarded(c, [&] {
         if (!c->have_sa || !c->have_lcp) fail(RS_ESTATE, "no structures on device");
         long long n = c->n;
-        long long *dtmp = (long long *)buf(c, B_I64A, 8 * (size_t)(n + 2));
-        RS_CUDA(cudaMemsetAsync(dtmp, 0, 8, c->stream));
-        widen_u32_to_i64(c, (const unsigned *)c->bufs[B_SA].p, dtmp + 1, n, 1);
-        d2h(c, sa, dtmp, 8 * (size_t)(n + 1));
-        RS_CUDA(cudaStreamSynchronize(c->stream));
+        sa[0] = rank[0] = lcp[0] = 0;
+        fetch_u32_as_i64(c, (long long *)sa + 1, (const unsigned *)c->bufs[B_SA].p, n, 1);
         ensure_isa(c);
-        widen_u32_to_i64(c, (const unsigned *)c->bufs[B_ISA].p, dtmp + 1, n, 1);
-        d2h(c, rank, dtmp, 8 * (size_t)(n + 1));
-        RS_CUDA(cudaStreamSynchronize(c->stream));
-        widen_u32_to_i64(c, (const unsigned *)c->bufs[B_LCP].p, dtmp + 1, n + 1, 0);
-        d2h(c, lcp, dtmp, 8 * (size_t)(n + 2));
-        RS_CUDA(cudaStreamSynchronize(c->stream));
+        fetch_u32_as_i64(c, (long long *)rank + 1, (const unsigned *)c->bufs[B_ISA].p, n, 1);
+        fetch_u32_as_i64(c, (long long *)lcp + 1, (const unsigned *)c->bufs[B_LCP].p, n + 1, 0);
         if (n == 0) lcp[1] = 0;
     });
 }
@@ -705,9 +707,8 @@ int rs_fetch_leftmost(rs_ctx *c, int64_t *starts, int64_t *lengths) {
     return guarded(c, [&] {
         if (c->out_mode != 0) fail(RS_ESTATE, "no leftmost results on device");
         long long n = c->n;
-        d2h(c, starts, c->bufs[B_OUT0].p, 8 * (size_t)(n + 1));
-        d2h(c, lengths, c->bufs[B_OUT1].p, 8 * (size_t)(n + 1));
-        RS_CUDA(cudaStreamSynchronize(c->stream));
+        fetch_i64(c, (long long *)starts, (const long long *)c->bufs[B_OUT0].p, n + 1, 1);
+        fetch_i64(c, (long long *)lengths, (const long long *)c->bufs[B_OUT1].p, n + 1, 0);
     });
 }
 
@@ -715,10 +716,9 @@ int rs_fetch_all(rs_ctx *c, int64_t *lengths, int64_t *offsets, int64_t *flat) {
     return guarded(c, [&] {
         if (c->out_mode != 1) fail(RS_ESTATE, "no all-ties results on device");
         long long n = c->n;
-        d2h(c, lengths, c->bufs[B_OUT0].p, 8 * (size_t)(n + 1));
-        d2h(c, offsets, c->bufs[B_OUT1].p, 8 * (size_t)(n + 2));
-        d2h(c, flat, c->bufs[B_FLAT].p, 8 * (size_t)c->total);
-        RS_CUDA(cudaStreamSynchronize(c->stream));
+        fetch_i64(c, (long long *)lengths, (const long long *)c->bufs[B_OUT0].p, n + 1, 0);
+        fetch_i64(c, (long long *)offsets, (const long long *)c->bufs[B_OUT1].p, n + 2, 2);
+        fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);
     });
 }
 
@@ -727,10 +727,7 @@ int rs_get_raw(rs_ctx *c, int64_t *raw) {
         bool used[RS_NUM_STAGES] = {};
         ensure_raw(c, used);
         long long n = c->n;
-        long long *dtmp = (long long *)buf(c, B_I64A, 8 * (size_t)(n + 2));
-        widen_u32_to_i64(c, (const unsigned *)c->bufs[B_RAW].p, dtmp, n + 1, 0);
-        d2h(c, raw, dtmp, 8 * (size_t)(n + 1));
-        RS_CUDA(cudaStreamSynchronize(c->stream));
+        fetch_u32_as_i64(c, (long long *)raw, (const unsigned *)c->bufs[B_RAW].p, n + 1, 0);
         raw[0] = 0;
     });
 }

@@ -69,6 +69,8 @@ enum BufId {
     B_V0,
     B_V1,
     B_SEND,      // distributed sort: (position, raw) entries bound for other ranks
+    B_XFER,      // host_io.cu: two-slot device ring of 32-bit wire words
+    B_XFER_ENDS, // host_io.cu: first / last value of every chunk
     B_COUNT
 };
 
@@ -90,6 +92,8 @@ struct rs_ctx {
     long long launches = 0;
     cudaEvent_t events[rsb::kMaxEvents] = {};
     void *small_host = nullptr;  // pinned scratch for scalar readbacks
+    void *xfer_host[2] = {nullptr, nullptr};        // host_io.cu pinned pipeline slots
+    cudaEvent_t xfer_ev[2] = {nullptr, nullptr};
     // pipeline state
     long long n = -1;
     bool have_text = false;

@@ -1,0 +1,320 @@
+// host_io.cu -- host <-> device transfers of the reference's int64 arrays.
+//
+// The API hands back (and takes) int64 numpy arrays in the reference layout
+// (query.py:130-168, suffixes.py:20-28): 8 bytes per value although every
+// value fits 32 bits (positions, lengths and starts are < 2^31; CSR offsets
+// are nondecreasing with small steps).  Measured on the B200 box
+// (tools/exp_d2h.py): a plain cudaMemcpy into a fresh pageable numpy array
+// runs at 4.1 GB/s, into pinned memory at 51 GB/s, and 16 host threads write
+// touched memory at ~90 GB/s (fresh pages ~40 GB/s).  So large transfers go
+// through a two-slot pipeline with 4 bytes per value on the wire:
+//   D2H: narrow kernel (int64 -> u32 word) into a device ring slot -> DMA into
+//        a pinned ring slot -> host threads widen into the caller's array,
+//        while the next slot's DMA runs;
+//   H2D: host threads narrow (range-checked) into a pinned slot -> DMA -> the
+//        caller's device u32 array (or, for bytes, a plain staged copy).
+// Offsets travel as their low 32 bits; each chunk's first value is fetched
+// in full beforehand and the host adds the (mod 2^32) differences, exact as
+// long as a chunk's span stays below 2^32 (checked; else plain int64 DMA).
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rsb {
+
+namespace {
+
+void h2d(rs_ctx *c, void *dst, const void *src, size_t bytes) {
+    if (bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+}
+void d2h(rs_ctx *c, void *dst, const void *src, size_t bytes) {
+    if (bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+}
+
+// ---- host thread pool: run(f) calls f(t, T) on T threads and waits ----------
+class Pool {
+  public:
+    static Pool &get() {
+        static Pool p;
+        return p;
+    }
+    int size() const { return (int)workers_.size() + 1; }
+    void run(const std::function<void(int, int)> &f) {
+        const int T = size();
+        if (T == 1) {
+            f(0, 1);
+            return;
+        }
+        {
+            std::unique_lock<std::mutex> lk(m_);
+            job_ = &f;
+            pending_ = T - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0, T);
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    Pool() {
+        int T = (int)std::thread::hardware_concurrency();
+        if (const char *e = std::getenv("RS_HOST_THREADS")) T = std::atoi(e);
+        T = std::max(1, std::min(T, 64));
+        for (int i = 1; i < T; ++i) workers_.emplace_back([this, i] { loop(i); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto &t : workers_) t.join();
+    }
+    void loop(int id) {
+        unsigned long long seen = 0;
+        for (;;) {
+            const std::function<void(int, int)> *f;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                f = job_;
+            }
+            (*f)(id, (int)workers_.size() + 1);
+            {
+                std::lock_guard<std::mutex> lk(m_);
+                if (--pending_ == 0) done_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int, int)> *job_ = nullptr;
+    int pending_ = 0;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+};
+
+inline void split(long long count, int t, int T, long long &a, long long &b) {
+    const long long per = (count + T - 1) / T;
+    a = std::min(count, per * t);
+    b = std::min(count, a + per);
+}
+
+constexpr long long kChunk = 16ll << 20;        // values per pipeline slot (64 MiB on the wire)
+constexpr size_t kMinStaged = 8u << 20;         // smaller arrays: one plain copy
+
+__global__ void k_narrow_words(const long long *__restrict__ src, unsigned *__restrict__ dst, long long count) {
+    long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < count) {
+        const longlong2 a = *reinterpret_cast<const longlong2 *>(src + i);
+        const longlong2 b = *reinterpret_cast<const longlong2 *>(src + i + 2);
+        *reinterpret_cast<uint4 *>(dst + i) = make_uint4((unsigned)a.x, (unsigned)a.y, (unsigned)b.x, (unsigned)b.y);
+    } else {
+        for (; i < count; ++i) dst[i] = (unsigned)src[i];
+    }
+}
+
+// every chunk's first and last value (offsets reconstruction / span check)
+__global__ void k_chunk_ends(const long long *__restrict__ src, long long count, long long chunk, long long nch,
+                             long long *__restrict__ out) {
+    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    long long a = c * chunk, b = (a + chunk < count ? a + chunk : count) - 1;
+    out[2 * c] = src[a];
+    out[2 * c + 1] = src[b];
+}
+
+struct Stage {
+    void **host;
+    cudaEvent_t *ev;
+};
+
+// the context's two pinned slots + events (allocated on first use, freed by
+// rs_destroy); waits until neither slot is still being copied
+Stage stage(rs_ctx *c) {
+    for (int i = 0; i < 2; ++i) {
+        if (!c->xfer_host[i]) RS_CUDA(cudaHostAlloc(&c->xfer_host[i], 4 * (size_t)kChunk, cudaHostAllocDefault));
+        if (!c->xfer_ev[i]) RS_CUDA(cudaEventCreateWithFlags(&c->xfer_ev[i], cudaEventDisableTiming));
+        RS_CUDA(cudaEventSynchronize(c->xfer_ev[i]));
+    }
+    return Stage{c->xfer_host, c->xfer_ev};
+}
+
+}  // namespace
+
+// Two-slot D2H pipeline: issue(a, len, slot) enqueues whatever produces the
+// chunk's 32-bit words on the stream and returns their device address; the
+// words are copied into the pinned slot, and widen(words, out, x, y, chunk)
+// runs on the host threads over [x, y) of the chunk while the next chunk's
+// copy is in flight.
+template <typename Issue, typename Widen>
+void pipeline_out(rs_ctx *c, long long count, Issue issue, Widen widen, long long *dst) {
+    const long long nch = (count + kChunk - 1) / kChunk;
+    Stage s = stage(c);
+    auto start = [&](long long i) {
+        const long long a = i * kChunk, len = std::min(kChunk, count - a);
+        const void *d = issue(a, len, (int)(i & 1));
+        RS_CUDA(cudaMemcpyAsync(s.host[i & 1], d, 4 * (size_t)len, cudaMemcpyDeviceToHost, c->stream));
+        RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
+    };
+    start(0);
+    if (nch > 1) start(1);
+    Pool &pool = Pool::get();
+    for (long long i = 0; i < nch; ++i) {
+        RS_CUDA(cudaEventSynchronize(s.ev[i & 1]));
+        const long long a = i * kChunk, len = std::min(kChunk, count - a);
+        const unsigned *w = (const unsigned *)s.host[i & 1];
+        long long *out = dst + a;
+        pool.run([&](int t, int T) {
+            long long x, y;
+            split(len, t, T, x, y);
+            if (y > x) widen(w, out, x, y, i);
+        });
+        if (i + 2 < nch) start(i + 2);
+    }
+}
+
+// D2H of `count` int64 values.  kind: 0 = values in [0, 2^32), 1 = values in
+// [-1, 2^31) (sign-extended), 2 = nondecreasing offsets.
+void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind) {
+    if (count <= 0) return;
+    if ((size_t)count * 8 < kMinStaged) {
+        d2h(c, dst, dsrc, 8 * (size_t)count);
+        RS_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    const long long nch = (count + kChunk - 1) / kChunk;
+    std::vector<long long> ends;
+    if (kind == 2) {
+        long long *d_ends = (long long *)buf(c, B_XFER_ENDS, 16 * (size_t)nch);
+        RS_LAUNCH(c, k_chunk_ends, grid_for(nch, 128), 128, 0, dsrc, count, kChunk, nch, d_ends);
+        ends.resize(2 * nch);
+        d2h(c, ends.data(), d_ends, 16 * (size_t)nch);
+        RS_CUDA(cudaStreamSynchronize(c->stream));
+        for (long long i = 0; i < nch; ++i)
+            if ((unsigned long long)(ends[2 * i + 1] - ends[2 * i]) >= (1ull << 32)) {  // span too wide
+                d2h(c, dst, dsrc, 8 * (size_t)count);
+                RS_CUDA(cudaStreamSynchronize(c->stream));
+                return;
+            }
+    }
+    unsigned *ring = (unsigned *)buf(c, B_XFER, 2 * 4 * (size_t)kChunk);
+    const long long *ends_p = ends.data();
+    pipeline_out(
+        c, count,
+        [&](long long a, long long len, int slot) {  // wire words of chunk [a, a + len) -> device slot
+            unsigned *d = ring + slot * kChunk;
+            RS_LAUNCH(c, k_narrow_words, grid_for((len + 3) / 4, 256), 256, 0, dsrc + a, d, len);
+            return (const void *)d;
+        },
+        [&](const unsigned *w, long long *out, long long x, long long y, long long chunk) {
+            if (kind == 0) {
+                for (long long j = x; j < y; ++j) out[j] = (long long)w[j];
+            } else if (kind == 1) {
+                for (long long j = x; j < y; ++j) out[j] = (long long)(int)w[j];
+            } else {
+                const long long first = ends_p[2 * chunk];
+                const unsigned w0 = w[0];
+                for (long long j = x; j < y; ++j) out[j] = first + (long long)(unsigned)(w[j] - w0);
+            }
+        },
+        dst);
+}
+
+// D2H of a device u32 array as int64 values + add (structures, raw LLR):
+// the 4-byte words go on the wire as they are.
+void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add) {
+    if (count <= 0) return;
+    pipeline_out(
+        c, count, [&](long long a, long long, int) { return (const void *)(dsrc + a); },
+        [&](const unsigned *w, long long *out, long long x, long long y, long long) {
+            for (long long j = x; j < y; ++j) out[j] = (long long)w[j] + add;
+        },
+        dst);
+}
+
+// H2D of `count` int64 values into a device u32 array, each checked to lie in
+// [lo, hi] and stored as value + add.  Returns false (nothing usable written)
+// if a value is out of range.
+bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long count, long long lo, long long hi,
+                    long long add) {
+    if (count <= 0) return true;
+    Stage s = stage(c);
+    Pool &pool = Pool::get();
+    const long long nch = (count + kChunk - 1) / kChunk;
+    std::atomic<bool> bad{false};
+    for (long long i = 0; i < nch; ++i) {
+        const long long a = i * kChunk, len = std::min(kChunk, count - a);
+        if (i >= 2) RS_CUDA(cudaEventSynchronize(s.ev[i & 1]));  // slot free again
+        unsigned *w = (unsigned *)s.host[i & 1];
+        const long long *in = src + a;
+        pool.run([&](int t, int T) {
+            long long x, y;
+            split(len, t, T, x, y);
+            bool ok = true;
+            for (long long j = x; j < y; ++j) {
+                const long long v = in[j];
+                ok &= (v >= lo) & (v <= hi);
+                w[j] = (unsigned)(v + add);
+            }
+            if (!ok) bad.store(true, std::memory_order_relaxed);
+        });
+        if (bad.load()) {
+            RS_CUDA(cudaStreamSynchronize(c->stream));
+            return false;
+        }
+        RS_CUDA(cudaMemcpyAsync(ddst + a, w, 4 * (size_t)len, cudaMemcpyHostToDevice, c->stream));
+        RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
+    }
+    RS_CUDA(cudaStreamSynchronize(c->stream));
+    return true;
+}
+
+// H2D of plain bytes (the text): host threads copy into the pinned slot, DMA
+// overlaps the next slot's copy.  Small copies go straight through.
+void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes) {
+    if (bytes < kMinStaged) {
+        h2d(c, ddst, src, bytes);
+        return;
+    }
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        h2d(c, ddst, src, bytes);  // already page-locked: direct DMA
+        return;
+    }
+    cudaGetLastError();
+    Stage s = stage(c);
+    Pool &pool = Pool::get();
+    const size_t ch = 4 * (size_t)kChunk;
+    const size_t nch = (bytes + ch - 1) / ch;
+    for (size_t i = 0; i < nch; ++i) {
+        const size_t a = i * ch, len = std::min(ch, bytes - a);
+        if (i >= 2) RS_CUDA(cudaEventSynchronize(s.ev[i & 1]));
+        char *w = (char *)s.host[i & 1];
+        const char *in = (const char *)src + a;
+        pool.run([&](int t, int T) {
+            long long x, y;
+            split((long long)len, t, T, x, y);
+            if (y > x) std::memcpy(w + x, in + x, (size_t)(y - x));
+        });
+        RS_CUDA(cudaMemcpyAsync((char *)ddst + a, w, len, cudaMemcpyHostToDevice, c->stream));
+        RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
+    }
+}
+
+}  // namespace rsb

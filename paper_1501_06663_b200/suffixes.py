@@ -37,9 +37,14 @@ def build_suffix_structures(text: Text) -> SuffixStructures:
     """SA, rank and LCP arrays of the text (suffixes.py:56-66), built on device."""
     data = _text_data(text)
     n = int(data.size)
-    sa = np.zeros(n + 1, dtype=np.int64)
-    rank = np.zeros(n + 1, dtype=np.int64)
-    lcp = np.zeros(n + 2, dtype=np.int64)
+    if n == 0:
+        z = np.zeros(1, dtype=np.int64)
+        return SuffixStructures(sa=z, rank=z.copy(), lcp=np.zeros(2, dtype=np.int64))
+    # every slot is written by the library (pads included); large arrays come
+    # from the caching host pool (csrc/host_io.cu pipelines the D2H into them)
+    sa = _native.out_array(n + 1, False)
+    rank = _native.out_array(n + 1, False)
+    lcp = _native.out_array(n + 2, False)
     if n > 0:
         ctx = _native.context()
         with ctx.lock:
