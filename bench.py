@@ -274,7 +274,7 @@ def run_single(args) -> None:
         ctx.call("rs_set_text", _native.u8(host_text), n)
         ctx.call("rs_build_structures")
         ctx.call("rs_get_structures", _native.i64(sa), _native.i64(rk), _native.i64(lc))
-        ctx.call("rs_set_structures", None, _native.i64(rk), _native.i64(lc), n)
+        ctx.call("rs_set_structures", _native.i64(sa), _native.i64(rk), _native.i64(lc), n)
 
         def q_step():  # llr.py:63-123 + query.py:187-215 from resident structures
             ctx.call("rs_clear_llr")
@@ -359,7 +359,7 @@ def run_single(args) -> None:
                    "timed": "raw LLR + compaction + all-ties query with the suffix structures given "
                             "(query.py:234; BASELINE.md section 2), int64 CSR answers written on device",
                    "structures": "built untimed on device, passed back in as the reference's int64 "
-                                 "SuffixStructures (rank, lcp)",
+                                 "SuffixStructures (sa, rank, lcp; sa checked once to invert rank)",
                    "parallelism": "single GPU",
                    "l2": "input 256 MiB > 126 MB L2; raw LLR, compaction and answers rebuilt each step",
                    "T": T},

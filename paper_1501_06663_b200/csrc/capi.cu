@@ -205,6 +205,7 @@ void d2h(rs_ctx *c, void *dst, const void *src, size_t bytes) {
 void invalidate(rs_ctx *c) {
     c->have_text = c->have_sa = c->have_lcp = c->have_raw = c->have_compact = false;
     c->sa_device_built = false;
+    c->sa_isa_consistent = false;
     c->raw_from_round0 = false;
     c->packed_bits = 0;
     c->isa_lazy = false;
@@ -240,7 +241,7 @@ void ensure_raw(rs_ctx *c, bool *used) {
     }
     Stage st(c, RS_STAGE_RAW_LLR);
     used[RS_STAGE_RAW_LLR] = true;
-    if (c->have_sa && c->sa_device_built)
+    if (c->have_sa && (c->sa_device_built || c->sa_isa_consistent))
         raw_from_sa_lcp(c, n, raw_slots(n));  // SA order + bucketed scatter (consistent structures)
     else
         raw_from_rank_lcp(c, n);  // reference formula on caller-given rank/lcp
@@ -549,6 +550,13 @@ int rs_set_structures(rs_ctx *c, const int64_t *sa, const int64_t *rank, const i
             if (!put_i64_as_u32(c, dlcp, (const long long *)lcp + 1, n + 1, 0, n, 0))
                 fail(RS_EINVAL, "lcp has values out of range");
         }
+        // The reference computes raw LLR from rank and lcp (_kernels_numba.py:33-38).
+        // When sa is given and is exactly the inverse of rank, the same values
+        // come from SA order (lcp read sequentially + one bucketed scatter)
+        // instead of two random lcp gathers per position; checked once here.
+        if (sa && n > 0)
+            c->sa_isa_consistent =
+                check_rank_inverse(c, (const unsigned *)c->bufs[B_SA].p, disa, n);
         RS_CUDA(cudaStreamSynchronize(c->stream));
         c->n = n;
         c->have_sa = sa != nullptr;

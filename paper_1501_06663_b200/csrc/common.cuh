@@ -121,6 +121,7 @@ struct rs_ctx {
     long long sa_final_depth = 0;          // sorted depth when prefix doubling stopped
     bool lcp_from_keys = false;
     bool sa_device_built = false;
+    bool sa_isa_consistent = false;          // caller sa/rank checked to be inverse permutations
     bool raw_from_round0 = false;
     long long tsv_bytes = 0;
     long long patch_slots = 0;              // tied slots of round 0 kept in B_PATCH

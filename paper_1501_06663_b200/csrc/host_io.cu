@@ -16,6 +16,8 @@
 // Offsets travel as their low 32 bits; each chunk's first value is fetched
 // in full beforehand and the host adds the (mod 2^32) differences, exact as
 // long as a chunk's span stays below 2^32 (checked; else plain int64 DMA).
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -68,7 +70,10 @@ class Pool {
 
   private:
     Pool() {
-        int T = (int)std::thread::hardware_concurrency();
+        // threads we may actually run on (cgroup / taskset), not the host's core count
+        cpu_set_t set;
+        int T = sched_getaffinity(0, sizeof(set), &set) == 0 ? CPU_COUNT(&set)
+                                                             : (int)std::thread::hardware_concurrency();
         if (const char *e = std::getenv("RS_HOST_THREADS")) T = std::atoi(e);
         T = std::max(1, std::min(T, 64));
         for (int i = 1; i < T; ++i) workers_.emplace_back([this, i] { loop(i); });

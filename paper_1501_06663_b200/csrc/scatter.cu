@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(kApplyNT) k_bucket_apply(const uint2 *__restri
                                                            unsigned *__restrict__ out2, int out2_shift) {
     const long long b = blockIdx.x / chunks_per_bucket;
     const long long chunk = blockIdx.x % chunks_per_bucket;
-    const long long count = cursor[b * kCursorStride];
+    long long count = cursor[b * kCursorStride];
+    if (count > (1ll << shift)) count = 1ll << shift;  // overfull bucket: non-injective dest (caller data)
     const long long begin = chunk * (kApplyNT * kApplyIPT);
     if (begin >= count) return;
     const uint2 *src = stage + (b << shift);
@@ -120,7 +121,37 @@ __global__ void __launch_bounds__(kRNT) k_pair_emit(const unsigned *__restrict__
     bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
 }
 
+__global__ void k_equal_u32(const unsigned *__restrict__ a, const unsigned *__restrict__ b, long long n,
+                            unsigned *err) {
+    long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4;
+    bool bad = false;
+    if (i + 3 < n) {
+        const uint4 x = *reinterpret_cast<const uint4 *>(a + i), y = *reinterpret_cast<const uint4 *>(b + i);
+        bad = (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+    } else {
+        for (; i < n; ++i) bad |= a[i] != b[i];
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
 }  // namespace
+
+// True iff isa is the inverse permutation of sa (both 0-based, n entries):
+// isa'[sa[r]] = r through the bucketed scatter into a cleared buffer (holes
+// and duplicates of a non-permutation stay 0xffffffff), then one coalesced
+// comparison with isa.
+bool check_rank_inverse(rs_ctx *c, const unsigned *sa, const unsigned *isa, long long n) {
+    if (n <= 0) return true;
+    unsigned *tmp = (unsigned *)buf(c, B_T0, sizeof(unsigned) * (size_t)(n + 4));
+    RS_CUDA(cudaMemsetAsync(tmp, 0xff, sizeof(unsigned) * (size_t)n, c->stream));
+    scatter_rank(c, sa, n, tmp);
+    unsigned *err = (unsigned *)((char *)buf(c, B_SMALL, 4096) + 192);
+    RS_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), c->stream));
+    RS_LAUNCH_B(c, 8.0 * n, k_equal_u32, grid_for((n + 3) / 4, 256), 256, 0, tmp, isa, n, err);
+    unsigned h = 0;
+    fetch_small(c, &h, err, sizeof(h));
+    return h == 0;
+}
 
 BucketEmit bucket_setup(rs_ctx *c, long long n_out, int slot, bool two) {
     // <= 256 buckets: a block's items spread over few buckets (long runs), and

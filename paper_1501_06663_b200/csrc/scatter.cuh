@@ -82,7 +82,10 @@ __device__ __forceinline__ void bucket_emit(const BucketEmit &be, const unsigned
     for (unsigned i = threadIdx.x; i < total; i += NT) {
         const unsigned d = sm.dest[i];
         const unsigned b = d >> be.shift;
-        const long long slot = ((long long)b << be.shift) + sm.gbase[b] + (i - sm.bstart[b]);
+        const unsigned within = sm.gbase[b] + (i - sm.bstart[b]);
+        // dest not injective (caller data): never write past the bucket's region
+        if (within >> be.shift) continue;
+        const long long slot = ((long long)b << be.shift) + within;
         be.stage[slot] = make_uint2(d, sm.val[i]);
         if (val2) be.stage2[slot] = sm.val2[i];
     }
@@ -97,6 +100,8 @@ void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n);
 void scatter_phi(rs_ctx *c, const unsigned *sa, long long n, unsigned *phi);
 // isa[sa[r]] = r through the bucketed scatter.
 void scatter_rank(rs_ctx *c, const unsigned *sa, long long n, unsigned *isa);
+// isa == inverse permutation of sa (0-based, n entries)?
+bool check_rank_inverse(rs_ctx *c, const unsigned *sa, const unsigned *isa, long long n);
 // out[dest[i]] = val[i], i < n; dest a permutation into [0, n_out).
 void scatter_by(rs_ctx *c, const unsigned *dest, const unsigned *val, long long n, unsigned *out, long long n_out);
 

@@ -535,3 +535,54 @@ def test_distributed_suffix_sort_declines_repetitive_text():
     from paper_1501_06663_b200 import distributed as D
     data = workloads.periodic_mutated(50_000, 3, period=7, rate=0.0)
     assert D.loopback_dist_all_positions(data, 2, "all") is None
+
+
+def test_given_sa_only_used_when_it_inverts_rank(rng):
+    """rs_set_structures with sa: raw LLR comes from SA order only when sa is
+    exactly the inverse of rank (checked on device); a permuted or
+    non-permutation sa must not change the answers, which the reference
+    derives from rank and lcp alone (_kernels_numba.py:33-38)."""
+    from paper_1501_06663_b200 import _native
+    ctx = _native.context()
+    data = workloads.iid_dna(200_000, 21)
+    n = data.size
+    s = rb.build_suffix_structures(rb.Text(data))
+    want = rb.all_positions(rb.Text(data), mode="all")
+    bad_perm = s.sa.copy()
+    bad_perm[[5, 9]] = bad_perm[[9, 5]]
+    dup = s.sa.copy()
+    dup[100:200] = dup[300]
+    for sa in (s.sa, bad_perm, dup):
+        sa = np.ascontiguousarray(sa, np.int64)
+        total = np.zeros(1, np.int64)
+        with ctx.lock:
+            ctx.call("rs_set_structures", _native.i64(sa), _native.i64(np.ascontiguousarray(s.rank)),
+                     _native.i64(np.ascontiguousarray(s.lcp)), n)
+            ctx.call("rs_query", 1, 1, _native.i64(total))
+            L = np.empty(n + 1, np.int64)
+            O = np.empty(n + 2, np.int64)
+            F = np.empty(int(total[0]), np.int64)
+            ctx.call("rs_fetch_all", _native.i64(L), _native.i64(O), _native.i64(F))
+        assert np.array_equal(L, want.lengths) and np.array_equal(O, want.offsets)
+        assert np.array_equal(F, want.flat_starts)
+
+
+def test_large_transfers_through_the_pipeline(rng):
+    """csrc/host_io.cu: results above the staging threshold travel as 32-bit
+    words and are widened on the host (offsets rebuilt from their low words);
+    pinned and pageable destinations, fresh and reused pool blocks."""
+    data = workloads.iid_dna(9_000_000, 5)
+    import oracle
+    os_ = oracle.build_suffix_structures(data, workers=8)
+    want = oracle.all_positions(data, mode="all", path="compact", workers=8, structures=os_)
+    for pinned in (False, True, False):
+        A = rb.all_positions(rb.Text(data), mode="all", pinned=pinned)
+        assert np.array_equal(A.lengths, want[0]) and np.array_equal(A.offsets, want[1])
+        assert np.array_equal(A.flat_starts, want[2])
+    L = rb.all_positions(rb.Text(data), mode="leftmost")
+    st, ln = oracle.all_positions(data, mode="leftmost", path="compact", workers=8, structures=os_)
+    assert np.array_equal(L.starts, st) and np.array_equal(L.lengths, ln)
+    s = rb.build_suffix_structures(rb.Text(data))
+    assert rb.verify_suffix_structures(rb.Text(data), s)
+    raw = rb.build_raw_llr(s)
+    assert np.array_equal(raw, oracle.build_raw_llr(s.rank, s.lcp, 8))
