@@ -208,6 +208,14 @@ int rs_set_compact_device(rs_ctx *ctx, int64_t m, int64_t n);
 /* cudaStream_t of the context (for torch.cuda.ExternalStream). */
 int rs_stream(rs_ctx *ctx, void **stream);
 int rs_query_shard(rs_ctx *ctx, int mode, int64_t lo, int64_t hi, int64_t *total);
+/* Position shard [lo, hi) (1-based) answered from the suffix structures on
+ * the device (rs_set_structures or rs_build_structures): raw LLR for the
+ * shard's slots and its left halo (slots >= lo - max LCP, the only ones that
+ * can reach lo) by the reference formula (_kernels_numba.py:33-38), then the
+ * fused compact scan.  Shard outputs as rs_query_shard (rebase / fetch with
+ * rs_shard_rebase, rs_fetch_shard).  Multi-GPU query-from-structures: every
+ * rank holds the structures and answers its own shard, no exchange. */
+int rs_query_structures_shard(rs_ctx *ctx, int mode, int64_t lo, int64_t hi, int64_t *total);
 /* Add `base` (the ties of all earlier shards) to the shard's offsets on device. */
 int rs_shard_rebase(rs_ctx *ctx, int64_t base);
 /* D2H of the shard results (a, b, flat as described above). */

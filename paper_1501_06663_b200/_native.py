@@ -87,6 +87,7 @@ SIGNATURES = {
     "rs_dist_apply": [_CTX, ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int64, ctypes.c_int64, _I64P],
     "rs_dist_scan": [_CTX, ctypes.c_int, ctypes.c_int64, _I64P],
     "rs_query_shard": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _I64P],
+    "rs_query_structures_shard": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _I64P],
     "rs_shard_rebase": [_CTX, ctypes.c_int64],
     "rs_fetch_shard": [_CTX, ctypes.c_int, _I64P, _I64P, _I64P],
 }

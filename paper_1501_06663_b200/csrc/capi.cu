@@ -18,6 +18,8 @@ void add_i64(rs_ctx *c, long long *d, long long count, long long add);
 void join_llrc(rs_ctx *c, const long long *d_starts, const long long *d_lengths, long long m, long long n);
 void validate_llrc(rs_ctx *c, long long m, long long n);
 void check_raw(rs_ctx *c, long long n);
+void raw_from_rank_lcp_range(rs_ctx *c, long long n, long long first, long long last);
+long long max_lcp(rs_ctx *c, long long n);
 void raw_llr_i64(rs_ctx *c, const long long *d_rank, const long long *d_lcp, long long n, long long *d_out);
 void flags_i64(rs_ctx *c, const long long *d_raw, long long n, long long *d_out);
 void scan_i64(rs_ctx *c, const long long *d_in, long long count, long long *d_out);
@@ -206,6 +208,7 @@ void invalidate(rs_ctx *c) {
     c->have_text = c->have_sa = c->have_lcp = c->have_raw = c->have_compact = false;
     c->sa_device_built = false;
     c->sa_isa_consistent = false;
+    c->max_lcp = -1;
     c->raw_from_round0 = false;
     c->packed_bits = 0;
     c->isa_lazy = false;
@@ -234,6 +237,7 @@ void ensure_raw(rs_ctx *c, bool *used) {
         used[RS_STAGE_LCP] = true;
         build_lcp(c, n);
         c->have_lcp = true;
+        c->max_lcp = -1;
         if (c->raw_from_round0) {  // the SA/LCP build already produced raw
             c->have_raw = true;
             return;
@@ -561,6 +565,7 @@ int rs_set_structures(rs_ctx *c, const int64_t *sa, const int64_t *rank, const i
         c->n = n;
         c->have_sa = sa != nullptr;
         c->have_lcp = true;
+        c->max_lcp = -1;
     });
 }
 
@@ -632,6 +637,7 @@ int rs_build_structures(rs_ctx *c) {
             build_lcp(c, n);
         }
         c->have_lcp = true;
+        c->max_lcp = -1;
         collect_stages(c, used);
     });
 }
@@ -770,6 +776,7 @@ int rs_clear_derived(rs_ctx *c) {
     return guarded(c, [&] {
         if (!c->have_text) fail(RS_ESTATE, "no text loaded");
         c->have_sa = c->have_lcp = c->have_raw = c->have_compact = false;
+        c->max_lcp = -1;
         c->out_mode = -1;
     });
 }
@@ -965,6 +972,45 @@ int rs_query_shard(rs_ctx *c, int mode, int64_t lo, int64_t hi, int64_t *total) 
     });
 }
 
+int rs_query_structures_shard(rs_ctx *c, int mode, int64_t lo, int64_t hi, int64_t *total) {
+    return guarded(c, [&] {
+        if (!c->have_lcp) fail(RS_ESTATE, "no suffix structures on device");
+        if (mode != RS_MODE_LEFTMOST && mode != RS_MODE_ALL) fail(RS_EINVAL, "unknown mode");
+        if (lo < 1 || hi < lo || hi > c->n + 1) fail(RS_ERANGE, "shard out of range");
+        const long long n = c->n;
+        bool used[RS_NUM_STAGES] = {};
+        if (c->isa_lazy) ensure_isa(c);
+        if (c->max_lcp < 0) c->max_lcp = max_lcp(c, n);
+        const long long cnt = hi - lo;
+        // raw slots that can cover [lo, hi): a slot i < lo reaches lo only if
+        // raw[i] > lo - i, and raw[i] <= max LCP (Lemma 1)
+        const long long first = std::max(1ll, lo - c->max_lcp);
+        {
+            Stage st(c, RS_STAGE_RAW_LLR);
+            used[RS_STAGE_RAW_LLR] = true;
+            if (cnt > 0) raw_from_rank_lcp_range(c, n, std::max(0ll, first - 1), hi - 1);
+        }
+        {
+            Stage st(c, RS_STAGE_QUERY);
+            used[RS_STAGE_QUERY] = true;
+            long long *o1 = (long long *)buf(c, B_OUT1, 8 * (size_t)(cnt + 2));
+            buf(c, B_OUT0, 8 * (size_t)(cnt + 1));
+            RS_CUDA(cudaMemsetAsync(o1, 0, 8, c->stream));
+            c->total = 0;
+            c->out_ref_layout = false;
+            const unsigned *raw = (const unsigned *)c->bufs[B_RAW].p;
+            if (cnt > 0 && !query_range(c, mode, RS_PATH_COMPACT, nullptr, 0, raw, lo, hi - 1, 0, cnt, first))
+                query_range(c, mode, RS_PATH_RAW, nullptr, 0, raw, lo, hi - 1, 0, cnt, first);
+            c->out_mode = mode;
+        }
+        collect_stages(c, used);
+        c->have_raw = c->have_compact = false;  // B_RAW holds only the shard's slots
+        c->shard_lo = lo;
+        c->shard_hi = hi;
+        if (total) *total = mode == RS_MODE_ALL ? c->total : 0;
+    });
+}
+
 int rs_shard_rebase(rs_ctx *c, int64_t base) {
     return guarded(c, [&] {
         if (c->out_mode != RS_MODE_ALL) fail(RS_ESTATE, "no all-ties shard results on device");
@@ -978,10 +1024,15 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
     return guarded(c, [&] {
         if (c->out_mode != mode) fail(RS_ESTATE, "no shard results of this mode on device");
         long long cnt = c->shard_hi - c->shard_lo;
-        d2h(c, a, c->bufs[B_OUT0].p, 8 * (size_t)cnt);
-        d2h(c, b, c->bufs[B_OUT1].p, 8 * (size_t)(mode == RS_MODE_ALL ? cnt + 1 : cnt));
-        if (mode == RS_MODE_ALL) d2h(c, flat, c->bufs[B_FLAT].p, 8 * (size_t)c->total);
-        RS_CUDA(cudaStreamSynchronize(c->stream));
+        const long long *o0 = (const long long *)c->bufs[B_OUT0].p, *o1 = (const long long *)c->bufs[B_OUT1].p;
+        if (mode == RS_MODE_ALL) {
+            fetch_i64(c, (long long *)a, o0, cnt, 0);
+            fetch_i64(c, (long long *)b, o1, cnt + 1, 2);
+            fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);
+        } else {
+            fetch_i64(c, (long long *)a, o0, cnt, 1);
+            fetch_i64(c, (long long *)b, o1, cnt, 0);
+        }
     });
 }
 

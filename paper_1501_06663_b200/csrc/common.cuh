@@ -121,7 +121,8 @@ struct rs_ctx {
     long long sa_final_depth = 0;          // sorted depth when prefix doubling stopped
     bool lcp_from_keys = false;
     bool sa_device_built = false;
-    bool sa_isa_consistent = false;          // caller sa/rank checked to be inverse permutations
+    bool sa_isa_consistent = false;
+    long long max_lcp = -1;                  // max of the resident LCP (-1: not computed)          // caller sa/rank checked to be inverse permutations
     bool raw_from_round0 = false;
     long long tsv_bytes = 0;
     long long patch_slots = 0;              // tied slots of round 0 kept in B_PATCH
@@ -260,8 +261,10 @@ __device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op) 
         u64 s;
         if (idx >= 0) {
             s = ld_relaxed(&status[idx]);
+            unsigned ns = 32;  // exponential backoff: a waiting warp issues few instructions
             while ((s >> 62) == 0) {
-                __nanosleep(20);
+                __nanosleep(ns);
+                ns = ns < 512 ? 2 * ns : ns;
                 s = ld_relaxed(&status[idx]);
             }
         } else {

@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(kNT) k_compact_raw(const unsigned *__restrict_
 // with isa 0-based ranks and lcp_d[r] = lcp(sa[r-1], sa[r]), lcp_d[0] = lcp_d[n] = 0.
 // 8 consecutive slots per thread so 16 independent random loads are in flight.
 __global__ void k_raw_from_isa_lcp(const unsigned *__restrict__ isa, const unsigned *__restrict__ lcp_d,
-                                   long long n, unsigned *__restrict__ raw) {
-    const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8;  // raw slots i0..i0+7
+                                   long long n, unsigned *__restrict__ raw, long long first = 0) {
+    const long long i0 = first + (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8;  // raw slots i0..i0+7
     if (i0 > n) return;
     unsigned r[8], a[8], b[8];
 #pragma unroll
@@ -272,6 +272,33 @@ long long compact_from_raw(rs_ctx *c, long long n) {
 size_t raw_slots(long long n) {
     long long tiles = (n + 1 + kTile - 1) / kTile;
     return (size_t)(tiles * kTile + 16);
+}
+
+// raw slots [first, last] only (a position shard and its left halo)
+void raw_from_rank_lcp_range(rs_ctx *c, long long n, long long first, long long last) {
+    unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots(n));
+    const long long cnt = last - first + 1;
+    if (cnt <= 0) return;
+    RS_LAUNCH_B(c, 16.0 * cnt, k_raw_from_isa_lcp, grid_for((cnt + 7) / 8, 256), 256, 0,
+                (const unsigned *)c->bufs[B_ISA].p, (const unsigned *)c->bufs[B_LCP].p, last, raw, first);
+}
+
+__global__ void k_max_u32(const unsigned *__restrict__ a, long long count, unsigned *out) {
+    unsigned v = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+        v = max(v, a[i]);
+    v = __reduce_max_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
+// max over the resident SA-order LCP (bounds every raw LLR value: a shard's halo)
+long long max_lcp(rs_ctx *c, long long n) {
+    unsigned *o = (unsigned *)((char *)buf(c, B_SMALL, 4096) + 320);
+    RS_CUDA(cudaMemsetAsync(o, 0, sizeof(unsigned), c->stream));
+    if (n > 0) RS_LAUNCH(c, k_max_u32, 4 * c->sm_count, 256, 0, (const unsigned *)c->bufs[B_LCP].p, n + 1, o);
+    unsigned h = 0;
+    fetch_small(c, &h, o, sizeof(h));
+    return (long long)h;
 }
 
 void raw_from_rank_lcp(rs_ctx *c, long long n) {
