@@ -549,292 +549,6 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
     query_tile<CandSoA, ALL>(c, x);
 }
 
-// ---------------------------------------------------------------------------
-// Record-chain scan (compact path, compaction fused; the default).
-//
-// Same staging and tile-local compaction as k_query_fused, but no
-// per-position walk over the window.  Per compacted entry t of the tile:
-//   ng[t]  = first u > t with len[u] >  len[t]   (next strictly greater)
-//   nge[t] = first u > t with len[u] >= len[t]   (next greater or equal)
-// (searched up to kChainD entries ahead).  For a window [wl, wh) of at most
-// kChainD entries the leftmost maximum is the end of the ng-chain from wl
-// that stays below wh (its records), and the ties are the nge-chain from
-// there: every entry of the window is <= the maximum, so the next entry >= it
-// inside the window is the next tie.  A position costs (records + ties) hops
-// -- ~2.5 + 1.8 on i.i.d. DNA -- instead of a walk over all ~6 (warp max ~10)
-// entries, and the tie list is the same chain again.  Longer windows
-// (repetitive text) walk directly.  Results are identical to Algorithms 2/4
-// (_kernels_numba.py:105-118, 158-195): leftmost max = first max in start
-// order, ties in increasing start order.
-// Lengths fit 16 bits here: the host takes this path only when every tile's
-// staged raw range is <= kFStage slots, and a raw value L spans L slots of
-// the range of the tile holding its last position.
-constexpr int kChainD = 32;
-constexpr unsigned short kNoIdx = 0xffff;
-constexpr int kCRegionB = 8 * kFStage;  // s_off, s_ln, s_ng, s_nge (u16 each)
-constexpr int kChainSmem = kFRegionA + kCRegionB + 2 * kFTiesCap;
-static_assert(kChainSmem + 128 <= 233472 / 8 - 1024, "8 CTAs per SM");
-
-template <bool ALL>
-__global__ void __launch_bounds__(kNT, 8) k_query_chain(const unsigned *__restrict__ raw, long long kb, long long ke,
-                                                     const long long *__restrict__ bounds, int out_off,
-                                                     long long *__restrict__ out0, long long *__restrict__ out1,
-                                                     long long *__restrict__ flat, long long flat_cap, u64 *status,
-                                                     long long tiles, unsigned long long *total_out,
-                                                     unsigned ties_cap) {
-    extern __shared__ __align__(128) unsigned char dsm[];
-    unsigned *s_raw = reinterpret_cast<unsigned *>(dsm);
-    unsigned short *s_lo = reinterpret_cast<unsigned short *>(dsm);  // after compaction (aliases s_raw)
-    unsigned short *s_hi = s_lo + kG;
-    unsigned *s_cnt = reinterpret_cast<unsigned *>(dsm + 4 * kG);
-    unsigned short *s_off = reinterpret_cast<unsigned short *>(dsm + kFRegionA);  // start - lo
-    unsigned short *s_ln = s_off + kFStage;
-    unsigned short *s_ng = s_ln + kFStage;
-    unsigned short *s_nge = s_ng + kFStage;
-    unsigned short *s_ties = reinterpret_cast<unsigned short *>(dsm + kFRegionA + kCRegionB);
-    __shared__ __align__(8) unsigned long long s_bar;
-    __shared__ unsigned s_warp[kNT / 32];
-    __shared__ u64 s_base;
-
-    const long long tile = blockIdx.x;  // dispatch-order assumption: see lookback_warp
-    const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];  // raw slots [lo, hi)
-    const long long tile_k0 = kb + tile * kG;
-    const int npos = (int)((ke - tile_k0 + 1) < kG ? (ke - tile_k0 + 1) : kG);
-    const int tk0 = (int)tile_k0, tk1 = (int)(tile_k0 + npos - 1);
-    const long long slot0 = tile_k0 - kb + out_off;
-
-    const long long a = (lo - 1) & ~3ll, b = (hi + 3) & ~3ll;  // stage raw[a, b), 16-byte aligned
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        const unsigned bytes = (unsigned)((b - a) * 4);
-        mbar_expect_tx(&s_bar, bytes);
-        tma_load_1d(s_raw, raw + a, bytes, &s_bar);
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-    // ---- tile-local compaction (flag = raw > 0 && raw >= previous raw), order kept ----
-    const int nr = (int)(hi - lo);
-    const int per = (nr + kNT - 1) / kNT;
-    const int o0 = threadIdx.x * per;
-    const unsigned *r0 = s_raw + (lo - a);  // r0[o] = raw[lo + o], r0[-1] = raw[lo - 1]
-    unsigned nf = 0;
-    for (int q = 0; q < per; ++q) {
-        const int o = o0 + q;
-        if (o < nr) nf += (r0[o] > 0u && r0[o] >= r0[o - 1]);
-    }
-    unsigned w;
-    const unsigned cnt = block_exclusive_sum<kNT>(nf, w, s_warp);
-    for (int q = 0; q < per; ++q) {
-        const int o = o0 + q;
-        if (o < nr && r0[o] > 0u && r0[o] >= r0[o - 1]) {
-            s_off[w] = (unsigned short)o;
-            s_ln[w++] = (unsigned short)r0[o];
-        }
-    }
-    __syncthreads();  // s_raw dead from here
-    for (int i = threadIdx.x; i < npos; i += kNT) {
-        s_lo[i] = (unsigned short)cnt;
-        s_hi[i] = 0;
-    }
-    // ---- chains: next greater / next greater-or-equal within kChainD entries ----
-    for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
-        const unsigned L = s_ln[t];
-        const unsigned lim = min(cnt, t + 1 + kChainD);
-        unsigned short ng = kNoIdx, nge = kNoIdx;
-#pragma unroll 1
-        for (unsigned u = t + 1; u < lim; ++u) {
-            const unsigned Lu = s_ln[u];
-            if (Lu >= L && nge == kNoIdx) nge = (unsigned short)u;
-            if (Lu > L) {
-                ng = (unsigned short)u;
-                break;
-            }
-        }
-        s_ng[t] = ng;
-        s_nge[t] = nge;
-    }
-    __syncthreads();
-    // ---- window bounds per position, filled by the entries (fill_windows) ----
-    {
-        const int base = (int)lo;
-        if (cnt * 8 < (unsigned)npos) {
-            for (int p = threadIdx.x; p < npos; p += kNT) {
-                const int k = tk0 + p;
-                unsigned x = 0, y = cnt;
-                while (x < y) {
-                    const unsigned mid = (x + y) >> 1;
-                    if (base + (int)s_off[mid] + (int)s_ln[mid] - 1 >= k) y = mid; else x = mid + 1;
-                }
-                s_lo[p] = (unsigned short)x;
-                y = cnt;
-                while (x < y) {
-                    const unsigned mid = (x + y) >> 1;
-                    if (base + (int)s_off[mid] <= k) x = mid + 1; else y = mid;
-                }
-                s_hi[p] = (unsigned short)x;
-            }
-        } else {
-            for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
-                const int st = base + (int)s_off[t];
-                const int e_t = st + (int)s_ln[t] - 1;
-                const int ep = t ? base + (int)s_off[t - 1] + (int)s_ln[t - 1] - 1 : tk0 - 1;
-                int x = ep + 1 > tk0 ? ep + 1 : tk0;
-                int y = e_t < tk1 ? e_t : tk1;
-#pragma unroll 1
-                for (int k = x; k <= y; ++k) s_lo[k - tk0] = (unsigned short)t;
-                const int sn = (t + 1 < cnt) ? base + (int)s_off[t + 1] : tk1 + 1;
-                x = st > tk0 ? st : tk0;
-                y = sn - 1 < tk1 ? sn - 1 : tk1;
-#pragma unroll 1
-                for (int k = x; k <= y; ++k) s_hi[k - tk0] = (unsigned short)(t + 1);
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- per position: leftmost max + tie count from the chains ----
-    unsigned short fidx[kPPT];
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x + j * kNT;
-        fidx[j] = kNoIdx;
-        if (p >= npos) continue;
-        const unsigned wl = s_lo[p], wh = s_hi[p];
-        unsigned M = 0, nt = 0, f = kNoIdx;
-        if (wl < wh) {
-            if (wh - wl <= (unsigned)kChainD) {
-                f = wl;
-#pragma unroll 1
-                for (unsigned u = s_ng[f]; u < wh; u = s_ng[u]) f = u;
-                M = s_ln[f];
-                nt = 1;
-#pragma unroll 1
-                for (unsigned u = s_nge[f]; u < wh; u = s_nge[u]) ++nt;
-            } else {
-#pragma unroll 1
-                for (unsigned t = wl; t < wh; ++t) {
-                    const unsigned L = s_ln[t];
-                    if (L > M) {
-                        M = L;
-                        f = t;
-                        nt = 1;
-                    } else if (L == M) {
-                        ++nt;
-                    }
-                }
-            }
-        }
-        fidx[j] = (unsigned short)f;
-        if (ALL) {
-            out0[slot0 + p] = M;
-            s_cnt[p] = nt;
-        } else {
-            out0[slot0 + p] = M ? lo + (long long)s_off[f] : -1ll;
-            out1[slot0 + p] = M;
-        }
-    }
-    if (!ALL) {
-        if (tile == 0 && threadIdx.x == 0 && out_off) {
-            out0[0] = -1;
-            out1[0] = 0;
-        }
-        return;
-    }
-
-    // ---- all ties: exclusive scan of the tile's counts (position order) ----
-    __syncthreads();
-    unsigned mine[kPPT], msum = 0;
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x * kPPT + j;
-        mine[j] = p < npos ? s_cnt[p] : 0;
-        msum += mine[j];
-    }
-    unsigned excl;
-    const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, s_warp);
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x * kPPT + j;
-        if (p < npos) s_cnt[p] = excl;
-        excl += mine[j];
-    }
-    __syncthreads();
-    // warp 0 resolves the tile's CSR base while the others list the ties
-    if (threadIdx.x < 32) {
-        u64 base = lookback_warp(status, tile, (u64)block_total, OpSum());
-        if (threadIdx.x == 0) {
-            s_base = base;
-            if (tile == tiles - 1) *total_out = base + block_total;
-        }
-    }
-    const bool staged = block_total <= ties_cap;
-    if (staged) {
-#pragma unroll
-        for (int j = 0; j < kPPT; ++j) {
-            const int p = threadIdx.x + j * kNT;
-            if (p >= npos || fidx[j] == kNoIdx) continue;
-            const unsigned wl = s_lo[p], wh = s_hi[p];
-            unsigned wpos = s_cnt[p];
-            if (wh - wl <= (unsigned)kChainD) {
-                unsigned u = fidx[j];
-                do {
-                    s_ties[wpos++] = (unsigned short)u;
-                    u = s_nge[u];
-                } while (u < wh);
-            } else {
-                const unsigned M = s_ln[fidx[j]];
-#pragma unroll 1
-                for (unsigned t = fidx[j]; t < wh; ++t)
-                    if (s_ln[t] == M) s_ties[wpos++] = (unsigned short)t;
-            }
-        }
-    }
-    __syncthreads();
-    const u64 tile_base = s_base;
-    if (tile == 0 && threadIdx.x == 0) {
-        if (out_off) {
-            out0[0] = 0;  // lengths[0]
-            out1[0] = 0;  // offsets[0]
-        }
-        out1[out_off] = 0;  // offsets of the first position
-    }
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x + j * kNT;
-        if (p < npos)  // offsets[k+1] = inclusive prefix
-            out1[slot0 + 1 + p] = (long long)(tile_base + ((p + 1 < npos) ? s_cnt[p + 1] : block_total));
-    }
-    if (staged && (long long)(tile_base + block_total) <= flat_cap) {
-        long long *const ft = flat + tile_base;
-        for (unsigned i = threadIdx.x; i < block_total; i += kNT) ft[i] = lo + (long long)s_off[s_ties[i]];
-        return;
-    }
-    // direct stores (tie list overflow or flat capacity exceeded: the host re-runs)
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-        const int p = threadIdx.x + j * kNT;
-        if (p >= npos || fidx[j] == kNoIdx) continue;
-        const unsigned wl = s_lo[p], wh = s_hi[p];
-        long long wpos = (long long)(tile_base + s_cnt[p]);
-        const unsigned M = s_ln[fidx[j]];
-        if (wh - wl <= (unsigned)kChainD) {
-            unsigned u = fidx[j];
-            do {
-                if (wpos < flat_cap) flat[wpos] = lo + (long long)s_off[u];
-                ++wpos;
-                u = s_nge[u];
-            } while (u < wh);
-        } else {
-#pragma unroll 1
-            for (unsigned t = fidx[j]; t < wh; ++t)
-                if (s_ln[t] == M) {
-                    if (wpos < flat_cap) flat[wpos] = lo + (long long)s_off[t];
-                    ++wpos;
-                }
-        }
-    }
-}
-
 // max over tiles of the staged raw range (hi - lo + 8) -> *out
 __global__ void k_max_span(const long long *__restrict__ bounds, long long tiles, unsigned long long *out) {
     long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -969,8 +683,6 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
         once_per_device(fattr, c->device, [] {
             RS_CUDA(cudaFuncSetAttribute(k_query_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
             RS_CUDA(cudaFuncSetAttribute(k_query_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
-            RS_CUDA(cudaFuncSetAttribute(k_query_chain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kChainSmem));
-            RS_CUDA(cudaFuncSetAttribute(k_query_chain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kChainSmem));
         });
     }
 
@@ -988,14 +700,8 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     // int64 outputs written once (leftmost 16 B/pos; all 16 B/pos + 8 B/tie).
     const double cand_bytes = (rawp || fused) ? 4.0 * (double)npos : 8.0 * (double)count;
     const double qbytes = cand_bytes + 16.0 * (double)npos;
-    // RS_SCAN=walk selects the per-position window walk (k_query_fused) for A/B runs
-    const char *scan_env = std::getenv("RS_SCAN");
-    const bool chain = !(scan_env && std::strcmp(scan_env, "walk") == 0);
     if (!all) {
-        if (fused && chain)
-            RS_LAUNCH_B(c, qbytes, (k_query_chain<false>), (unsigned)tiles, kNT, kChainSmem, d_raw, kb, ke, bounds,
-                        out_off, out0, out1, nullptr, 0, nullptr, tiles, tot, 0u);
-        else if (fused)
+        if (fused)
             RS_LAUNCH_B(c, qbytes, (k_query_fused<false>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
                         out_off, out0, out1, nullptr, 0, nullptr, nullptr, tiles, tot, 0u);
         else if (rawp)
@@ -1024,12 +730,8 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
                 const long v = std::strtol(e, nullptr, 10);
                 if (v >= 0 && v < ties_cap) ties_cap = (unsigned)v;
             }
-            if (chain)
-                RS_LAUNCH_B(c, qbytes, (k_query_chain<true>), (unsigned)tiles, kNT, kChainSmem, d_raw, kb, ke, bounds,
-                            out_off, out0, out1, flat, (long long)cap_slots, s.status, tiles, tot, ties_cap);
-            else
-                RS_LAUNCH_B(c, qbytes, (k_query_fused<true>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
-                            out_off, out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot, ties_cap);
+            RS_LAUNCH_B(c, qbytes, (k_query_fused<true>), (unsigned)tiles, kNT, kFusedSmem, d_raw, kb, ke, bounds,
+                        out_off, out0, out1, flat, (long long)cap_slots, s.counter, s.status, tiles, tot, ties_cap);
         }
         else if (rawp)
             RS_LAUNCH_B(c, qbytes, (k_query<true, true>), (unsigned)tiles, kNT, kQuerySmem, d_e, d_raw, kb, ke, bounds, out_off,

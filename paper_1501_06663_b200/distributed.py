@@ -135,6 +135,109 @@ def gather_shards(n: int, mode: str, lo: int, hi: int, a, b, flat, total_all: in
 
 
 # ---------------------------------------------------------------------------------------
+# shared host output: every rank D2Hs its shard into its slice of ONE host buffer
+# (SURVEY 8(e) collectives, step 4) -- no gather through rank 0's GPU / PCIe link
+# ---------------------------------------------------------------------------------------
+def answer_layout(n: int, mode: str, total: int) -> dict:
+    """Element offsets of the reference arrays inside one int64 buffer."""
+    if mode == "leftmost":
+        return {"starts": (0, n + 1), "lengths": (n + 1, n + 1)}
+    return {"lengths": (0, n + 1), "offsets": (n + 1, n + 2), "flat": (2 * n + 3, max(total, 0))}
+
+
+def layout_views(buf: np.ndarray, n: int, mode: str, total: int) -> dict:
+    return {k: buf[o:o + c] for k, (o, c) in answer_layout(n, mode, total).items()}
+
+
+def shard_views(views: dict, mode: str, lo: int, hi: int, base: int, t_shard: int):
+    """The slices one rank's shard fills (rs_fetch_shard's a, b, flat):
+    all: lengths[lo:hi], offsets[lo:hi+1] (offsets[lo] = the shard's base, written
+    identically by the previous shard), flat[base:base+T_r]; leftmost: starts, lengths."""
+    if mode == "leftmost":
+        return views["starts"][lo:hi], views["lengths"][lo:hi], None
+    return views["lengths"][lo:hi], views["offsets"][lo:hi + 1], views["flat"][base:base + t_shard]
+
+
+def fill_pads(views: dict, mode: str) -> None:
+    """Slot-0 pads of the reference layout (query.py:174-175, 190-204)."""
+    if mode == "leftmost":
+        views["starts"][0] = -1
+        views["lengths"][0] = 0
+    else:
+        views["lengths"][0] = 0
+        views["offsets"][0] = 0
+        views["offsets"][1] = 0
+
+
+class SharedHostBuffer:
+    """One int64 host buffer mapped by every rank of the node (/dev/shm file,
+    unlinked as soon as every rank has mapped it).  Raises MemoryError when
+    /dev/shm cannot hold it (callers fall back to the NCCL gather)."""
+
+    def __init__(self, nelems: int, group=None, root: str = "/dev/shm"):
+        import mmap
+        import uuid
+
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        nbytes = max(8 * int(nelems), 8)
+        name = [None, None]
+        if rank == 0:
+            try:
+                st = os.statvfs(root)
+                free = st.f_bavail * st.f_frsize
+            except OSError:
+                free = 0
+            if free >= nbytes + (64 << 20):
+                path = os.path.join(root, f"repeatscan_{os.getpid()}_{uuid.uuid4().hex[:12]}")
+                fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+                os.ftruncate(fd, nbytes)
+                os.close(fd)
+                name = [path, None]
+            else:
+                name = [None, f"{root} has {free} bytes free, {nbytes} needed"]
+        dist.broadcast_object_list(name, src=0, group=group)
+        if name[0] is None:
+            raise MemoryError(name[1])
+        fd = os.open(name[0], os.O_RDWR)
+        try:
+            self._mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+        finally:
+            os.close(fd)
+        dist.barrier(group=group)
+        if rank == 0:
+            os.unlink(name[0])
+        self.array = np.frombuffer(self._mm, dtype=np.int64, count=int(nelems))
+
+
+def fetch_shard_shared(ctx, n: int, mode: str, lo: int, hi: int, base: int, totals: list[int],
+                       group=None):
+    """Every rank copies its (rebased) shard from its GPU into its slice of one
+    shared host buffer (csrc/host_io.cu pipeline, its own PCIe link and host
+    threads); rank 0 returns the reference dataclass backed by that buffer."""
+    import torch.distributed as dist
+
+    from paper_1501_06663_b200.query import AllAnswers, LeftmostAnswers
+    rank = dist.get_rank(group)
+    T_all = int(sum(totals)) if mode == "all" else 0
+    views = layout_views(SharedHostBuffer(sum(c for _, c in answer_layout(n, mode, T_all).values()),
+                                          group).array, n, mode, T_all)
+    a, b, f = shard_views(views, mode, lo, hi, base, int(totals[rank]) if mode == "all" else 0)
+    if hi > lo:
+        null = ctypes.POINTER(ctypes.c_int64)()
+        ctx.call("rs_fetch_shard", _native.MODE[mode], _native.i64(a), _native.i64(b),
+                 _native.i64(f) if f is not None and f.size else null)
+    if rank == 0:
+        fill_pads(views, mode)
+    dist.barrier(group=group)
+    if rank != 0:
+        return None
+    if mode == "leftmost":
+        return LeftmostAnswers(starts=views["starts"], lengths=views["lengths"])
+    return AllAnswers(lengths=views["lengths"], offsets=views["offsets"], flat_starts=views["flat"])
+
+
+# ---------------------------------------------------------------------------------------
 # device path
 # ---------------------------------------------------------------------------------------
 class _CudaView:
@@ -224,6 +327,62 @@ def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None
     return out
 
 
+def structures_query_shard(ctx, n: int, mode: str, group=None, device=None) -> tuple:
+    """Query step from the suffix structures resident on every rank's GPU:
+    rank r answers shard_range(n, world, r) (rs_query_structures_shard: raw LLR
+    of its slots and left halo, fused scan -- no data exchange), tie totals are
+    all-gathered and the shard's CSR offsets rebased on device.
+    Returns (lo, hi, base, totals)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    lo, hi = shard_range(n, world, rank)
+    total = np.zeros(1, np.int64)
+    ctx.call("rs_query_structures_shard", _native.MODE[mode], lo, hi, _native.i64(total))
+    if mode != "all":
+        return lo, hi, 0, [0] * world
+    totals = exchange_totals(int(total[0]), group, device)
+    base = tie_bases(totals)[rank]
+    ctx.call("rs_shard_rebase", base)
+    return lo, hi, base, totals
+
+
+def replicated_all_positions(data: np.ndarray | None, mode: str = "all", group=None):
+    """API-level multi-GPU all_positions (query.py:218-239) over the ranks of
+    `group`: rank 0's host text is copied to its GPU and broadcast over NVLink,
+    every rank builds the suffix structures on its own GPU (no exchange during
+    the sort), answers its position shard from them, and D2Hs its rebased shard
+    into one shared host buffer.  Rank 0 returns the reference dataclass."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    dev_index = torch.cuda.current_device()
+    device = torch.device("cuda", dev_index)
+    ctx = _native.context(dev_index)
+    with ctx.lock:
+        nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device=device)
+        dist.broadcast(nn, src=0, group=group)
+        n = int(nn.item())
+        if rank == 0:
+            ctx.call("rs_set_text", _native.u8(np.ascontiguousarray(data, dtype=np.uint8)), n)
+        tv = _view(ctx, _native.BUF_TEXT, n + 128, "|u1", device)[:n]
+        torch.cuda.synchronize(device)
+        dist.broadcast(tv, src=0, group=group)
+        torch.cuda.synchronize(device)
+        ctx.call("rs_set_text_device", n)
+        ctx.call("rs_build_structures")
+        lo, hi, base, totals = structures_query_shard(ctx, n, mode, group, device)
+        try:
+            return fetch_shard_shared(ctx, n, mode, lo, hi, base, totals, group)
+        except MemoryError:
+            cnt = hi - lo
+            a = _view(ctx, _native.BUF_OUT0, cnt, "<i8", device)
+            b = _view(ctx, _native.BUF_OUT1, cnt + 1, "<i8", device)
+            f = _view(ctx, _native.BUF_FLAT, int(totals[rank]), "<i8", device) if mode == "all" else None
+            ctx.synchronize()
+            out = gather_shards(n, mode, lo, hi, a, b, f, int(sum(totals)), base, group, device)
+            return to_answers(out, mode) if rank == 0 else None
+
+
 def _to_host(t):
     """One D2H of a device tensor into a pooled pinned numpy array (full PCIe rate)."""
     import torch
@@ -251,17 +410,19 @@ def to_answers(out, mode: str):
 # bench (torchrun, N > 1)
 # ---------------------------------------------------------------------------------------
 def bench_main(args) -> None:
-    """torchrun bench (N > 1), strong scaling over one text.
+    """torchrun bench (N > 1): the same metric and config as bench.py at N = 1,
+    strong scaling over one text.
 
-    value: device-resident step.  Preferred path (DNA-like
-    text): every rank holds the text and sorts one segment of the suffix
-    array, raw LLR is exchanged all-to-all into position shards and every
-    rank scans its shard, keeping its CSR shard in its own HBM.  Texts
-    outside that regime: rank 0 builds SA -> LLRc, LLRc is broadcast and the
-    ranks scan position shards.  CUDA events on the library
-    stream, max over ranks.
-    e2e: the API-level call -- text from rank 0's host, the same path, shards
-    gathered to rank 0 over NVLink and one D2H into the reference int64 arrays.
+    value: n / the query step from suffix structures resident on every GPU
+    (BASELINE.md section 2 like-for-like step: raw LLR + compaction + all-ties
+    scan), rank r answering position shard r (rs_query_structures_shard: its
+    slots plus a left halo of max-LCP slots, no data exchange), tie totals
+    all-gathered over NCCL and the shard's CSR rebased.  CUDA events on each
+    rank's library stream, max over ranks.
+    e2e: replicated_all_positions -- the API call from rank 0's host text:
+    NVLink broadcast of the text, every rank builds the structures on its GPU
+    and answers its shard, every rank D2Hs its shard into one shared host
+    buffer (wall clock across barriers, max over ranks).
     """
     import json
     import sys
@@ -271,95 +432,100 @@ def bench_main(args) -> None:
 
     from paper_1501_06663_b200 import workloads
 
-    # stdout carries exactly one JSON line: everything else written to fd 1
-    # (e.g. the NCCL version banner at communicator creation) goes to stderr
+    # stdout carries exactly one JSON line; NCCL's own lines (NCCL_DEBUG=INFO
+    # shows the communicator's rank count) go to stderr
     sys.stdout.flush()
     json_fd = os.dup(1)
     os.dup2(2, 1)
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    # host threads of the transfer pipeline: this rank's share of the node
+    os.environ.setdefault("RS_HOST_THREADS", str(max(1, (os.cpu_count() or 1) // max(1, local_world))))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
     device = torch.device("cuda", local)
+    gen = workloads.make(args.config, args.n) if rank == 0 else None
     data = None
     if rank == 0:
-        gen = workloads.make(args.config, args.n)
-        data = _native.pinned_pool.empty(int(gen.size), np.uint8)  # pinned: the e2e H2D runs at PCIe rate
-        data[:] = gen
-    nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device=device)
-    dist.broadcast(nn, src=0)
-    n = int(nn.item())
+        data = np.array(gen)  # the caller's pageable text
     ctx = _native.context(local)
-    # text resident on every rank (the distributed sort reads it everywhere)
+
+    # ---- value: query from resident structures, position shards ----
     with ctx.lock:
-        tv = _view(ctx, _native.BUF_TEXT, n, "|u1", device)[:n]
+        nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device=device)
+        dist.broadcast(nn, src=0)
+        n = int(nn.item())
         if rank == 0:
-            tv.copy_(torch.from_numpy(data))
+            ctx.call("rs_set_text", _native.u8(data), n)
+        tv = _view(ctx, _native.BUF_TEXT, n + 128, "|u1", device)[:n]
+        torch.cuda.synchronize(device)
         dist.broadcast(tv, src=0)
         torch.cuda.synchronize(device)
         ctx.call("rs_set_text_device", n)
-    use_dist = dist_sa_all_positions(None, n, "all", resident=True, gather=False) is not None
-    if not use_dist and rank == 0:  # rank 0 keeps the text for the LLRc path
-        with ctx.lock:
-            ctx.call("rs_set_text", _native.u8(data), n)
+        ctx.call("rs_build_structures")  # untimed, like the reference arm's structures
 
-    def step():
-        if use_dist:
-            dist_sa_all_positions(None, n, "all", resident=True, gather=False)
-        else:
-            sharded_all_positions(data, "all", resident=True, gather=False)
+        def step():
+            return structures_query_shard(ctx, n, "all", None, device)
 
-    for _ in range(args.warmup):
-        step()
-    dist.barrier()
-    torch.cuda.synchronize()
-    l0 = ctx.launches()
-    ctx.record(0)
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize()
-    ctx.record(1)
-    ms = ctx.elapsed_ms(0, 1) / args.steps
-    launches = (ctx.launches() - l0) / args.steps
+        for _ in range(args.warmup):
+            step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        l0 = ctx.launches()
+        ctx.record(0)
+        for _ in range(args.steps):
+            lo, hi, base, totals = step()
+        ctx.record(1)
+        ctx.synchronize()
+        ms = ctx.elapsed_ms(0, 1) / args.steps
+        launches = ctx.launches() - l0
+        stages = ctx.stage_times()
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    lt = torch.tensor([launches], dtype=torch.float64, device=device)
+    lt = torch.tensor([float(launches)], dtype=torch.float64, device=device)
     dist.all_reduce(lt, op=dist.ReduceOp.SUM)
-    # e2e: text H2D on rank 0 + the whole path + gather + final D2H of the CSR
+    T = int(sum(totals))
+
+    # ---- e2e: the API-level call with host buffers ----
     e2e = []
     res = None
-    for i in range(args.warmup + max(1, args.steps)):  # warm-up fills the pinned result pool
-        res = out = None
+    for i in range(args.warmup + max(1, args.steps)):
+        res = None
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = (dist_sa_all_positions(data, n, "all") if use_dist else sharded_all_positions(data, "all"))
-        res = to_answers(out, "all") if rank == 0 else None
+        res = replicated_all_positions(data if rank == 0 else None, "all")
         torch.cuda.synchronize()
         dist.barrier()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         if i >= args.warmup:
-            e2e.append(time.perf_counter() - t0)
+            e2e.append(float(dt.item()))
     if rank == 0:
-        T = int(res.flat_starts.size)
-        par = (f"distributed suffix sort x{world}: SA segments by top key digit, raw LLR all-to-all into "
-               f"position shards, per-shard scan; CSR shards stay on their GPUs" if use_dist else
-               f"position shards x{world} (SA/LLRc on rank 0, NCCL broadcast; CSR shards stay on their GPUs)")
+        assert int(res.flat_starts.size) == T, (res.flat_starts.size, T)
         line = {
             "metric": "positions/sec, all-longest-repeat query, n=256M DNA, 1/2/4/8 B200 vs CPU",
             "value": n / (ms * 1e-3), "unit": "positions/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8 text / u32 device indices / int64 answers",
-            "data": "synthetic",
+            "vs_baseline": None, "dtype": "u32 device indices / int64 answers", "data": "synthetic",
             "config": {"workload": args.config, "n": n, "mode": "all", "path": "compact",
-                       "parallelism": par,
-                       "l2": "input 256 MiB > 126 MB L2; all arrays rebuilt each step",
+                       "timed": "raw LLR + compaction + all-ties query from resident suffix structures "
+                                "(query.py:234), per rank one position shard; tie totals all-gathered "
+                                "(NCCL) and CSR offsets rebased on device",
+                       "parallelism": f"position shards x{world} (engine._chunks), structures on every GPU",
+                       "l2": "input 256 MiB > 126 MB L2; raw LLR, compaction and answers rebuilt each step",
                        "T": T},
-            "gpu_launches": int(round(float(lt.item()) * args.steps)),
+            "gpu_launches": int(round(float(lt.item()))),
+            "stages_ms_rank0": stages,
             "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": n,
                     "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
-                    "path": ("dist_sa_all_positions" if use_dist else "sharded_all_positions")
-                            + " + NCCL gather to rank 0 + D2H"},
+                    "ms_per_step": 1e3 * float(np.mean(e2e)),
+                    "path": "replicated_all_positions: text H2D on rank 0 + NCCL broadcast, suffix "
+                            "structures + shard query on every GPU, per-rank D2H into one shared host "
+                            "buffer (/dev/shm), max over ranks"},
         }
         os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
@@ -576,7 +742,7 @@ def dist_sa_all_positions(data: np.ndarray | None, n: int, mode: str = "all", gr
     kw = dict(dtype=torch.int64, device=device)
     with ctx.lock:
         if not resident:
-            tv = _view(ctx, _native.BUF_TEXT, n, "|u1", device)[:n]
+            tv = _view(ctx, _native.BUF_TEXT, n + 128, "|u1", device)[:n]
             if rank == 0:
                 tv.copy_(torch.from_numpy(np.ascontiguousarray(data, dtype=np.uint8)), non_blocking=True)
             dist.broadcast(tv, src=0, group=group)

@@ -127,3 +127,65 @@ def test_dist_halo_partners_skip_empty_shards():
     assert dist_halo_fits(10_000, 5, 4096) and not dist_halo_fits(10_000, 5, 4097)
     # the last non-empty shard never sends a halo, its size does not bound it
     assert dist_halo_fits(10_000, 3, 4000)
+
+
+def _shared_worker(rank, world, port, data, q):
+    """Every rank writes its shard's slices of ONE /dev/shm buffer (what
+    rs_fetch_shard does from its GPU); rank 0 reads the whole answer back."""
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = data.size
+        wl, wo, wf = oracle.all_positions(data, mode="all")
+        ls, ll = oracle.all_positions(data, mode="leftmost")
+        lo, hi = D.shard_range(n, world, rank)
+        totals = D.exchange_totals(int(wo[hi] - wo[lo]))
+        base = D.tie_bases(totals)[rank]
+        assert base == wo[lo]
+        out = {}
+        for mode in ("all", "leftmost"):
+            T = sum(totals) if mode == "all" else 0
+            buf = D.SharedHostBuffer(sum(c for _, c in D.answer_layout(n, mode, T).values()))
+            views = D.layout_views(buf.array, n, mode, T)
+            a, b, f = D.shard_views(views, mode, lo, hi, base, totals[rank])
+            if mode == "all":  # rebased shard: lengths, offsets[lo..hi], ties
+                a[:] = wl[lo:hi]
+                b[:] = wo[lo:hi + 1]
+                f[:] = wf[wo[lo]:wo[hi]]
+            else:
+                a[:] = ls[lo:hi]
+                b[:] = ll[lo:hi]
+            if rank == 0:
+                D.fill_pads(views, mode)
+            dist.barrier()
+            out[mode] = {k: v.copy() for k, v in views.items()}
+            dist.barrier()
+        if rank == 0:
+            A, L = out["all"], out["leftmost"]
+            ok = (np.array_equal(A["lengths"], wl) and np.array_equal(A["offsets"], wo)
+                  and np.array_equal(A["flat"], wf) and np.array_equal(L["starts"], ls)
+                  and np.array_equal(L["lengths"], ll))
+            q.put(("ok" if ok else "mismatch", 0))
+    except Exception as e:
+        q.put((f"error: {e!r}", rank))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shared_host_output_assembles_full_answer(world):
+    from paper_1501_06663_b200 import workloads
+    data = workloads.planted_dna(6000, 9, family_len=50)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shared_worker, args=(r, world, port, data, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    status, _ = q.get(timeout=10)
+    assert status == "ok", status
+    assert all(p.exitcode == 0 for p in procs)
