@@ -192,7 +192,10 @@ def run_reference(args) -> None:
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
-TRAFFIC_JSON = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+PROFILES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+TRAFFIC_JSON = next((os.path.join(PROFILES, r, "traffic.json") for r in ("r02", "r01")
+                     if os.path.exists(os.path.join(PROFILES, r, "traffic.json"))),
+                    os.path.join(PROFILES, "r02", "traffic.json"))
 
 
 def committed_traffic(kernel: str):
@@ -205,7 +208,8 @@ def committed_traffic(kernel: str):
         return None, None
     if not rec:
         return None, None
-    return rec["dram_bytes_per_launch"], f"profiles/r01/{rec['report']} (dram__bytes_read.sum + dram__bytes_write.sum)"
+    rnd = os.path.basename(os.path.dirname(TRAFFIC_JSON))
+    return rec["dram_bytes_per_launch"], f"profiles/{rnd}/{rec['report']} (dram__bytes_read.sum + dram__bytes_write.sum)"
 
 
 def roofline_of(profile: list[dict], steps: int) -> tuple[dict, list[dict]]:

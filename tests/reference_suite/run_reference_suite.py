@@ -7,12 +7,10 @@ it is read from /root/reference/pkg/tests when present, else from the
 git-ignored copy baseline/_ref/tests that tools/stage_reference_tests.sh
 makes in the build container (it travels to the GPU box with the snapshot).
 ``import repeatscan`` resolves to this package through repeatscan_alias.py.
-Deselected, with reasons:
-  * test_backends.py -- the numba/numpy backend selector (_backend.py), out
-    of scope (the north star forbids multi-backend dispatch);
-  * tests that run ``python -m repeatscan`` in a subprocess (the CLI of this
-    package is ``python -m paper_1501_06663_b200``; its flags, formats and exit
-    codes are covered by tests/test_cli_gpu.py).
+Deselected, with the reason: test_backends.py -- the numba/numpy backend
+SELECTOR (_backend.py:10-34 env handling), out of scope (the
+north star forbids multi-backend dispatch).  ``python -m repeatscan`` in the
+suite's subprocesses runs this package's CLI through shim/repeatscan.
 Exit status is pytest's.
 """
 
@@ -41,7 +39,7 @@ def main(argv: list[str]) -> int:
         print("reference test suite not found (run tools/stage_reference_tests.sh)", file=sys.stderr)
         return 5
     env = dict(os.environ)
-    env["PYTHONPATH"] = os.pathsep.join([str(HERE), str(REPO), env.get("PYTHONPATH", "")])
+    env["PYTHONPATH"] = os.pathsep.join([str(HERE), str(HERE / "shim"), str(REPO), env.get("PYTHONPATH", "")])
     cmd = [sys.executable, "-m", "pytest", "-p", "repeatscan_alias", "-p", "no:cacheprovider",
            "--rootdir", str(d), str(d), "--ignore", str(d / "test_backends.py"), *argv]
     return subprocess.call(cmd, env=env, cwd=str(d.parent) if os.access(d.parent, os.W_OK) else "/tmp")

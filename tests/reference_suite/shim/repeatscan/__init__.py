@@ -1,0 +1,23 @@
+"""Shim package: ``import repeatscan`` (and ``python -m repeatscan``) resolve to
+paper_1501_06663_b200 -- only on the PYTHONPATH of run_reference_suite.py, so
+the reference's own tests, including those that start ``python -m repeatscan``
+in a subprocess, exercise this package through the drop-in boundary."""
+
+import importlib
+import sys
+
+_MODULES = {
+    "repeatscan": "paper_1501_06663_b200",
+    "repeatscan.engine": "paper_1501_06663_b200.engine",
+    "repeatscan.llr": "paper_1501_06663_b200.llr",
+    "repeatscan.query": "paper_1501_06663_b200.query",
+    "repeatscan.suffixes": "paper_1501_06663_b200.suffixes",
+    "repeatscan.text": "paper_1501_06663_b200.text",
+    "repeatscan.stats": "paper_1501_06663_b200.stats",
+    "repeatscan.oracle": "paper_1501_06663_b200.bruteforce",
+    "repeatscan.cli": "paper_1501_06663_b200.cli",
+    "repeatscan._backend": "paper_1501_06663_b200._backend",
+}
+
+for _alias, _real in _MODULES.items():
+    sys.modules[_alias] = importlib.import_module(_real)

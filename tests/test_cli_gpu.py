@@ -94,3 +94,25 @@ def test_tsv_digest_matches_reference_1mb(tmp_path, capsys, mode):
         code, _, _ = run_cli(capsys, "query", "--mode", mode, "--path", path, "--output", dest, p)
         assert code == 0
         assert hashlib.sha256(dest.read_bytes()).hexdigest()[:16] == rec[f"{mode}_tsv"]
+
+
+def test_reference_test_suite_runs_against_this_package():
+    """The reference's own pytest suite (pkg/tests: suffixes, llr, query,
+    engine, stats, oracle, text, cli, acceptance) through ``import repeatscan``
+    -> this package (tests/reference_suite).  The suite is read from the
+    git-ignored baseline/_ref/tests staged in the build container (it is not
+    part of this repository's history); skipped where it was not staged."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    runner = Path(__file__).resolve().parent / "reference_suite" / "run_reference_suite.py"
+    sys.path.insert(0, str(runner.parent))
+    try:
+        import run_reference_suite as rrs
+    finally:
+        sys.path.pop(0)
+    if rrs.suite_dir() is None:
+        pytest.skip("reference test suite not staged (tools/stage_reference_tests.sh)")
+    proc = subprocess.run([sys.executable, str(runner), "-q", "-p", "no:randomly"],
+                          capture_output=True, text=True, timeout=1800)
+    assert proc.returncode == 0, proc.stdout[-4000:] + proc.stderr[-2000:]
