@@ -246,14 +246,21 @@ __device__ __forceinline__ u64 warp_reduce(u64 v, Op op) {
 // fuzzers) but which is not a documented guarantee -- do not run those two
 // under MPS / green-context SM partitioning without switching them back to
 // the atomic tile counter.
+// published = true: the caller already stored the tile's aggregate (or, for
+// tile 0, its inclusive prefix) with lookback_publish, earlier, so that
+// successors waiting on it are released before this tile starts waiting.
+__device__ __forceinline__ void lookback_publish(u64 *status, long long tile, u64 aggregate) {
+    st_relaxed(&status[tile], (tile == 0 ? kFlagPre : kFlagAgg) | (aggregate & kValMask));
+}
+
 template <typename Op>
-__device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op) {
+__device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op, bool published = false) {
     const int lane = threadIdx.x & 31;
     if (tile == 0) {
-        if (lane == 0) st_relaxed(&status[0], kFlagPre | (aggregate & kValMask));
+        if (lane == 0 && !published) st_relaxed(&status[0], kFlagPre | (aggregate & kValMask));
         return Op::identity;
     }
-    if (lane == 0) st_relaxed(&status[tile], kFlagAgg | (aggregate & kValMask));
+    if (lane == 0 && !published) st_relaxed(&status[tile], kFlagAgg | (aggregate & kValMask));
     u64 exclusive = Op::identity;
     long long base = tile - 1;
     while (true) {

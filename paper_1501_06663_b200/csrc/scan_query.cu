@@ -246,6 +246,10 @@ __device__ __forceinline__ void query_tile(const C &c, const TileCtx<IdxT> &x) {
     }
     unsigned excl;
     const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, x.s_warp);
+    // publish the tile's aggregate at once (successors stop waiting on it),
+    // but resolve this tile's own base only after listing the ties: by then
+    // the predecessors have had the listing's time to publish theirs
+    if (threadIdx.x == 0) lookback_publish(x.status, x.tile, (u64)block_total);
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
         const int p = threadIdx.x * kPPT + j;
@@ -253,17 +257,10 @@ __device__ __forceinline__ void query_tile(const C &c, const TileCtx<IdxT> &x) {
         excl += mine[j];
     }
     __syncthreads();
-    // Warp 0 resolves the tile's global base (decoupled look-back) while the
-    // other warps already list the tile's ties in shared memory as candidate
-    // indices in output order; after the barrier the list is written out
-    // coalesced.  Tiles whose ties overflow the list write directly.
-    if (threadIdx.x < 32) {
-        u64 base = lookback_warp(x.status, x.tile, (u64)block_total, OpSum());
-        if (threadIdx.x == 0) {
-            *x.s_base = base;
-            if (x.tile == x.tiles - 1) *x.total_out = base + block_total;
-        }
-    }
+    // Every warp lists its positions' ties in shared memory (candidate indices
+    // in output order); then warp 0 resolves the tile's global base (decoupled
+    // look-back); after the barrier the list is written out coalesced.  Tiles
+    // whose ties overflow the list write directly.
     const bool staged = x.s_ties != nullptr && block_total <= x.ties_cap;
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
@@ -289,6 +286,13 @@ __device__ __forceinline__ void query_tile(const C &c, const TileCtx<IdxT> &x) {
 #pragma unroll 1
             for (unsigned t = wl; t < wh; ++t)
                 if (c.len(t) == bl) x.s_ties[w++] = (unsigned short)t;
+        }
+    }
+    if (threadIdx.x < 32) {
+        u64 base = lookback_warp(x.status, x.tile, (u64)block_total, OpSum(), true);
+        if (threadIdx.x == 0) {
+            *x.s_base = base;
+            if (x.tile == x.tiles - 1) *x.total_out = base + block_total;
         }
     }
     __syncthreads();

@@ -586,3 +586,57 @@ def test_large_transfers_through_the_pipeline(rng):
     assert rb.verify_suffix_structures(rb.Text(data), s)
     raw = rb.build_raw_llr(s)
     assert np.array_equal(raw, oracle.build_raw_llr(s.rank, s.lcp, 8))
+
+
+@pytest.mark.parametrize("structures_from", ["device", "caller"])
+def test_structures_shards_assemble_to_full_answer(structures_from):
+    """rs_query_structures_shard (multi-GPU query from resident structures):
+    each shard computes raw LLR for its slots plus a max-LCP left halo and
+    scans; stitched shards == the full answer (fused path, and the raw-path
+    fallback of long repeats: Fibonacci)."""
+    from paper_1501_06663_b200 import _native
+    from paper_1501_06663_b200 import distributed as D
+    ctx = _native.context()
+    for data in (workloads.iid_dna(250_000, 31), workloads.planted_dna(300_000, 9, family_len=200),
+                 workloads.english_like(200_000, 4), workloads.fibonacci_mutated(150_000, 5, rate=1e-3)):
+        n = data.size
+        st = oracle.build_suffix_structures(data, workers=8)
+        want_l, want_o, want_f = oracle.all_positions(data, mode="all", workers=8, structures=st)
+        want_s, want_len = oracle.all_positions(data, mode="leftmost", workers=8, structures=st)
+        with ctx.lock:
+            if structures_from == "device":
+                ctx.call("rs_set_text", _native.u8(data), n)
+                ctx.call("rs_build_structures")
+            else:
+                ctx.call("rs_set_structures", _native.i64(st[0]), _native.i64(st[1]), _native.i64(st[2]), n)
+        for world in (1, 2, 3, 7):
+            lengths = np.zeros(n + 1, np.int64)
+            offsets = np.zeros(n + 2, np.int64)
+            starts = np.full(n + 1, -1, np.int64)
+            llen = np.zeros(n + 1, np.int64)
+            flats, base = [], 0
+            for r in range(world):
+                lo, hi = D.shard_range(n, world, r)
+                with ctx.lock:
+                    tot = np.zeros(1, np.int64)
+                    ctx.call("rs_query_structures_shard", 1, lo, hi, _native.i64(tot))
+                    ctx.call("rs_shard_rebase", base)
+                    a = np.zeros(hi - lo, np.int64)
+                    b = np.zeros(hi - lo + 1, np.int64)
+                    f = np.zeros(int(tot[0]), np.int64)
+                    ctx.call("rs_fetch_shard", 1, _native.i64(a), _native.i64(b), _native.i64(f))
+                    ctx.call("rs_query_structures_shard", 0, lo, hi, _native.i64(tot))
+                    s_ = np.zeros(hi - lo, np.int64)
+                    l_ = np.zeros(hi - lo, np.int64)
+                    ctx.call("rs_fetch_shard", 0, _native.i64(s_), _native.i64(l_), _native.i64(f[:0]))
+                assert b[0] == base
+                lengths[lo:hi] = a
+                offsets[lo + 1:hi + 1] = b[1:]
+                flats.append(f)
+                base += f.size
+                starts[lo:hi] = s_
+                llen[lo:hi] = l_
+            assert np.array_equal(lengths, want_l), world
+            assert np.array_equal(offsets, want_o), world
+            assert np.array_equal(np.concatenate(flats), want_f), world
+            assert np.array_equal(starts, want_s) and np.array_equal(llen, want_len), world
