@@ -346,7 +346,9 @@ __device__ __noinline__ static u64 lookback_warp_wide(u64 *st, long long tiles, 
 }
 
 // Block-wide exclusive sum of one u32 per thread; returns the block total.
-template <int NT>
+// kTrailingSync = false: the caller never rewrites s_warp before its next
+// __syncthreads (saves the closing barrier).
+template <int NT, bool kTrailingSync = true>
 __device__ __forceinline__ unsigned block_exclusive_sum(unsigned v, unsigned &excl,
                                                         unsigned *s_warp /*[NT/32]*/) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -371,7 +373,7 @@ __device__ __forceinline__ unsigned block_exclusive_sum(unsigned v, unsigned &ex
     unsigned warp_base = warp ? s_warp[warp - 1] : 0;
     excl = warp_base + x - v;
     unsigned total = s_warp[NT / 32 - 1];
-    __syncthreads();
+    if (kTrailingSync) __syncthreads();
     return total;
 }
 

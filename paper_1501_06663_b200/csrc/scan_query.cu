@@ -131,6 +131,21 @@ __device__ __forceinline__ void fill_windows(const C &c, unsigned cnt, int tile_
             s_hi[p] = (IdxT)a;
         }
     } else {
+        // every position gets both bounds (no prior initialisation needed):
+        // lo = cnt after the last end, hi = 0 before the first start
+        if (cnt == 0) {
+            for (int p = threadIdx.x; p < npos; p += kNT) {
+                s_lo[p] = (IdxT)0;
+                s_hi[p] = (IdxT)0;
+            }
+        } else if (threadIdx.x == 0) {
+            const int el = c.end(cnt - 1);
+#pragma unroll 1
+            for (int k = (el + 1 > tile_k0 ? el + 1 : tile_k0); k <= tile_k1; ++k) s_lo[k - tile_k0] = (IdxT)cnt;
+            const int s0 = (int)c.start(0);
+#pragma unroll 1
+            for (int k = tile_k0; k < s0 && k <= tile_k1; ++k) s_hi[k - tile_k0] = (IdxT)0;
+        }
         for (unsigned t = threadIdx.x; t < cnt; t += kNT) {
             const int ep = t ? c.end(t - 1) : tile_k0 - 1;
             const int e_t = c.end(t);
@@ -245,7 +260,7 @@ __device__ __forceinline__ void query_tile(const C &c, const TileCtx<IdxT> &x) {
         msum += mine[j];
     }
     unsigned excl;
-    const unsigned block_total = block_exclusive_sum<kNT>(msum, excl, x.s_warp);
+    const unsigned block_total = block_exclusive_sum<kNT, false>(msum, excl, x.s_warp);
     // publish the tile's aggregate at once (successors stop waiting on it),
     // but resolve this tile's own base only after listing the ties: by then
     // the predecessors have had the listing's time to publish theirs
@@ -481,6 +496,7 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ unsigned s_tile;
     __shared__ unsigned s_warp[kNT / 32];
+    __shared__ unsigned s_warp_c[kNT / 32];  // the compaction scan's own (no barrier between the scans)
     __shared__ u64 s_base;
 
     // tile = blockIdx.x also for the look-back of the all variant (blocks
@@ -532,7 +548,7 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
         if (o < nr) nf += (r0[o] > 0u && r0[o] >= r0[o - 1]);
     }
     unsigned w;
-    const unsigned cnt = block_exclusive_sum<kNT>(nf, w, s_warp);
+    const unsigned cnt = block_exclusive_sum<kNT, false>(nf, w, s_warp_c);
     for (int q = 0; q < per; ++q) {
         const int o = o0 + q;
         if (o < nr && r0[o] > 0u && r0[o] >= r0[o - 1]) {
@@ -541,12 +557,7 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
         }
     }
     x.cnt = cnt;
-    __syncthreads();  // s_raw dead from here: the window bounds take its place
-    for (int i = threadIdx.x; i < x.npos; i += kNT) {
-        x.s_lo[i] = (unsigned short)cnt;
-        x.s_hi[i] = 0;
-    }
-    __syncthreads();
+    __syncthreads();  // s_raw dead from here: the window bounds take its place (fill_windows writes all)
     CandSoA c;
     c.st = s_st;
     c.ln = s_ln;
