@@ -116,5 +116,6 @@ if __name__ == "__main__":
     for nm in names:
         fn = {"reference": from_reference, "oracle32": from_oracle32}[source]
         r = fn(nm)
-        _save(nm if source == "reference" else f"{nm}", r)
+        key = os.environ.get("FULLSIZE_KEY", nm)
+        _save(key, r)
         print(json.dumps({nm: r}), flush=True)
