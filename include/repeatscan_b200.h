@@ -257,6 +257,21 @@ int rs_dist_apply(rs_ctx *ctx, int32_t rank, int32_t world, const void *recv, in
                   int64_t *info);
 int rs_dist_scan(rs_ctx *ctx, int mode, int64_t halo, int64_t *total);
 
+/* ---- NCCL inside the library ------------------------------
+ * The multi-GPU data plane runs as NCCL collectives on each context's stream
+ * between the library's device buffers.  Rank 0 creates the 128-byte id
+ * (rs_nccl_unique_id) and hands it to the other ranks by any channel
+ * (torch.distributed in distributed.py); every rank then calls rs_nccl_init.
+ *   rs_nccl_broadcast_text  the text (RS_BUF_TEXT, n bytes) from `root` to
+ *                           every rank; leaves the text loaded (as rs_set_text)
+ *   rs_nccl_allgather_i64   one int64 per rank (the shards' tie totals) ->
+ *                           out[world] in rank order on every rank */
+int rs_nccl_unique_id(uint8_t *id128);
+int rs_nccl_init(rs_ctx *ctx, const uint8_t *id128, int32_t rank, int32_t world);
+int rs_nccl_destroy(rs_ctx *ctx);
+int rs_nccl_broadcast_text(rs_ctx *ctx, int64_t n, int32_t root);
+int rs_nccl_allgather_i64(rs_ctx *ctx, int64_t value, int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

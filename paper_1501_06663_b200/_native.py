@@ -89,6 +89,11 @@ SIGNATURES = {
     "rs_query_shard": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _I64P],
     "rs_query_structures_shard": [_CTX, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _I64P],
     "rs_shard_rebase": [_CTX, ctypes.c_int64],
+    "rs_nccl_unique_id": [ctypes.c_void_p],
+    "rs_nccl_init": [_CTX, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32],
+    "rs_nccl_destroy": [_CTX],
+    "rs_nccl_broadcast_text": [_CTX, ctypes.c_int64, ctypes.c_int32],
+    "rs_nccl_allgather_i64": [_CTX, ctypes.c_int64, _I64P],
     "rs_fetch_shard": [_CTX, ctypes.c_int, _I64P, _I64P, _I64P],
 }
 _RESTYPES = {"rs_version": ctypes.c_char_p, "rs_last_error": ctypes.c_char_p}

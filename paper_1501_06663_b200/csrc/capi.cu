@@ -49,6 +49,12 @@ bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long c
 void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes);
 void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add);
 
+void nccl_unique_id(unsigned char *out);
+void nccl_init(rs_ctx *c, const unsigned char *id_bytes, int rank, int world);
+void nccl_destroy(rs_ctx *c);
+void nccl_broadcast_text(rs_ctx *c, long long n, int root);
+void nccl_allgather_i64(rs_ctx *c, long long value, long long *out);
+
 void fail(int code, const std::string &msg) { throw RsError{code, msg}; }
 
 void check_cuda(cudaError_t e, const char *what, const char *file, int line) {
@@ -314,6 +320,12 @@ int rs_destroy(rs_ctx *c) {
     for (int i = 0; i < kMaxEvents; ++i)
         if (c->events[i]) cudaEventDestroy(c->events[i]);
     for (auto e : c->prof_events) cudaEventDestroy(e);
+    if (c->nccl_comm) {
+        try {
+            nccl_destroy(c);
+        } catch (...) {
+        }
+    }
     if (c->small_host) cudaFreeHost(c->small_host);
     for (int i = 0; i < 2; ++i) {
         if (c->xfer_host[i]) cudaFreeHost(c->xfer_host[i]);
@@ -1034,6 +1046,44 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
             fetch_i64(c, (long long *)b, o1, cnt, 0);
         }
     });
+}
+
+// ---- NCCL inside the library (collectives.cu) ---------------------------------------
+
+int rs_nccl_unique_id(uint8_t *id) {
+    if (!id) return RS_EINVAL;
+    try {
+        nccl_unique_id(id);
+        return RS_OK;
+    } catch (const RsError &e) {
+        fprintf(stderr, "rs_nccl_unique_id: %s\n", e.msg.c_str());
+        return e.code;
+    }
+}
+
+int rs_nccl_init(rs_ctx *c, const uint8_t *id, int32_t rank, int32_t world) {
+    return guarded(c, [&] {
+        if (!id) fail(RS_EINVAL, "null NCCL id");
+        nccl_init(c, id, rank, world);
+    });
+}
+
+int rs_nccl_destroy(rs_ctx *c) {
+    return guarded(c, [&] { nccl_destroy(c); });
+}
+
+int rs_nccl_broadcast_text(rs_ctx *c, int64_t n, int32_t root) {
+    return guarded(c, [&] {
+        check_n(n);
+        nccl_broadcast_text(c, n, root);
+        invalidate(c);
+        c->n = n;
+        c->have_text = true;
+    });
+}
+
+int rs_nccl_allgather_i64(rs_ctx *c, int64_t value, int64_t *out) {
+    return guarded(c, [&] { nccl_allgather_i64(c, value, (long long *)out); });
 }
 
 int rs_set_text_device(rs_ctx *c, int64_t n) {

@@ -93,6 +93,8 @@ struct rs_ctx {
     cudaEvent_t events[rsb::kMaxEvents] = {};
     void *small_host = nullptr;  // pinned scratch for scalar readbacks
     void *xfer_host[2] = {nullptr, nullptr};        // host_io.cu pinned pipeline slots
+    void *nccl_comm = nullptr;                      // collectives.cu (ncclComm_t)
+    int nccl_rank = 0, nccl_world = 1;
     cudaEvent_t xfer_ev[2] = {nullptr, nullptr};
     // pipeline state
     long long n = -1;

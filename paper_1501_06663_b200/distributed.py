@@ -327,6 +327,45 @@ def sharded_all_positions(data: np.ndarray | None, mode: str = "all", group=None
     return out
 
 
+def library_comm(ctx, group=None) -> bool:
+    """The library's own NCCL communicator for `group` (csrc/collectives.cu),
+    created once per context: rank 0's 128-byte ncclUniqueId travels over
+    torch.distributed (bootstrap only); every collective of the data plane
+    then runs inside the library on its stream.  False for non-NCCL groups
+    (gloo: host-logic tests), which keep the torch collectives."""
+    import torch.distributed as dist
+    if dist.get_backend(group) != "nccl":
+        return False
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    key = (world, tuple(dist.get_process_group_ranks(group)) if group is not None else None)
+    if getattr(ctx, "_nccl_key", None) == key:
+        return True
+    idb = [None]
+    if rank == 0:
+        raw = (ctypes.c_uint8 * 128)()
+        rc = ctx.lib.rs_nccl_unique_id(raw)
+        if rc != _native.RS_OK:
+            raise _native.RepeatscanError(f"rs_nccl_unique_id failed with status {rc}")
+        idb = [bytes(raw)]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(idb, src=src, group=group)
+    arr = (ctypes.c_uint8 * 128).from_buffer_copy(idb[0])
+    ctx.call("rs_nccl_init", arr, rank, world)
+    ctx._nccl_key = key
+    return True
+
+
+def allgather_i64(ctx, value: int, group=None, device=None) -> list[int]:
+    """One int64 per rank, rank order: NCCL inside the library when the group
+    is NCCL, else the torch collective (gloo)."""
+    import torch.distributed as dist
+    if library_comm(ctx, group):
+        out = np.zeros(dist.get_world_size(group), np.int64)
+        ctx.call("rs_nccl_allgather_i64", int(value), _native.i64(out))
+        return [int(v) for v in out]
+    return exchange_totals(int(value), group, device)
+
+
 def structures_query_shard(ctx, n: int, mode: str, group=None, device=None) -> tuple:
     """Query step from the suffix structures resident on every rank's GPU:
     rank r answers shard_range(n, world, r) (rs_query_structures_shard: raw LLR
@@ -340,7 +379,7 @@ def structures_query_shard(ctx, n: int, mode: str, group=None, device=None) -> t
     ctx.call("rs_query_structures_shard", _native.MODE[mode], lo, hi, _native.i64(total))
     if mode != "all":
         return lo, hi, 0, [0] * world
-    totals = exchange_totals(int(total[0]), group, device)
+    totals = allgather_i64(ctx, int(total[0]), group, device)
     base = tie_bases(totals)[rank]
     ctx.call("rs_shard_rebase", base)
     return lo, hi, base, totals
@@ -359,16 +398,17 @@ def replicated_all_positions(data: np.ndarray | None, mode: str = "all", group=N
     device = torch.device("cuda", dev_index)
     ctx = _native.context(dev_index)
     with ctx.lock:
-        nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device=device)
-        dist.broadcast(nn, src=0, group=group)
-        n = int(nn.item())
+        n = allgather_i64(ctx, int(data.size) if rank == 0 else 0, group, device)[0]
         if rank == 0:
             ctx.call("rs_set_text", _native.u8(np.ascontiguousarray(data, dtype=np.uint8)), n)
-        tv = _view(ctx, _native.BUF_TEXT, n + 128, "|u1", device)[:n]
-        torch.cuda.synchronize(device)
-        dist.broadcast(tv, src=0, group=group)
-        torch.cuda.synchronize(device)
-        ctx.call("rs_set_text_device", n)
+        if library_comm(ctx, group):  # NCCL broadcast inside the library, device buffer to device buffer
+            ctx.call("rs_nccl_broadcast_text", n, 0)
+        else:
+            tv = _view(ctx, _native.BUF_TEXT, n + 128, "|u1", device)[:n]
+            torch.cuda.synchronize(device)
+            dist.broadcast(tv, src=0, group=group)
+            torch.cuda.synchronize(device)
+            ctx.call("rs_set_text_device", n)
         ctx.call("rs_build_structures")
         lo, hi, base, totals = structures_query_shard(ctx, n, mode, group, device)
         try:
@@ -433,7 +473,7 @@ def bench_main(args) -> None:
     from paper_1501_06663_b200 import workloads
 
     # stdout carries exactly one JSON line; NCCL's own lines (NCCL_DEBUG=INFO
-    # shows the communicator's rank count) go to stderr
+    # shows the communicators' rank counts, torch's and the library's) go to stderr
     sys.stdout.flush()
     json_fd = os.dup(1)
     os.dup2(2, 1)
@@ -453,16 +493,10 @@ def bench_main(args) -> None:
 
     # ---- value: query from resident structures, position shards ----
     with ctx.lock:
-        nn = torch.tensor([int(data.size) if rank == 0 else 0], dtype=torch.int64, device=device)
-        dist.broadcast(nn, src=0)
-        n = int(nn.item())
+        n = allgather_i64(ctx, int(data.size) if rank == 0 else 0, None, device)[0]
         if rank == 0:
             ctx.call("rs_set_text", _native.u8(data), n)
-        tv = _view(ctx, _native.BUF_TEXT, n + 128, "|u1", device)[:n]
-        torch.cuda.synchronize(device)
-        dist.broadcast(tv, src=0)
-        torch.cuda.synchronize(device)
-        ctx.call("rs_set_text_device", n)
+        ctx.call("rs_nccl_broadcast_text", n, 0)  # NCCL inside the library (library_comm above)
         ctx.call("rs_build_structures")  # untimed, like the reference arm's structures
 
         def step():

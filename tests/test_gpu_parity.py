@@ -393,6 +393,20 @@ def test_distributed_single_rank_nccl():
         # outside the distributed regime it declines (caller falls back)
         rep = workloads.periodic_mutated(60_000, 3, period=7, rate=0.0)
         assert D.dist_sa_all_positions(rep, int(rep.size), "all") is None
+        # the library's own NCCL communicator (csrc/collectives.cu): text
+        # broadcast + tie-total all-gather inside the library, shards written
+        # into the shared host buffer -- the multi-GPU API path
+        from paper_1501_06663_b200 import _native
+        ctx = _native.context()
+        assert D.library_comm(ctx) and D.allgather_i64(ctx, 12345) == [12345]
+        for data in (workloads.planted_dna(200_000, 3, family_len=100),
+                     workloads.fibonacci_mutated(120_000, 5, rate=1e-3)):
+            st = oracle.build_suffix_structures(data, workers=8)
+            for mode in ("all", "leftmost"):
+                res = D.replicated_all_positions(data, mode)
+                want = oracle.all_positions(data, mode=mode, workers=8, structures=st)
+                got = (res.lengths, res.offsets, res.flat_starts) if mode == "all" else (res.starts, res.lengths)
+                assert all(np.array_equal(g, w) for g, w in zip(got, want)), mode
     finally:
         dist.destroy_process_group()
 
