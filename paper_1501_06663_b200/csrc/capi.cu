@@ -331,6 +331,8 @@ int rs_destroy(rs_ctx *c) {
         if (c->xfer_host[i]) cudaFreeHost(c->xfer_host[i]);
         if (c->xfer_ev[i]) cudaEventDestroy(c->xfer_ev[i]);
     }
+    if (c->xfer_side_ev) cudaEventDestroy(c->xfer_side_ev);
+    if (c->xfer_side) cudaStreamDestroy(c->xfer_side);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return RS_OK;

@@ -96,6 +96,8 @@ struct rs_ctx {
     void *nccl_comm = nullptr;                      // collectives.cu (ncclComm_t)
     int nccl_rank = 0, nccl_world = 1;
     cudaEvent_t xfer_ev[2] = {nullptr, nullptr};
+    cudaStream_t xfer_side = nullptr;                // host_io.cu direct-DMA side stream
+    cudaEvent_t xfer_side_ev = nullptr;
     // pipeline state
     long long n = -1;
     bool have_text = false;

@@ -194,10 +194,47 @@ void pipeline_out(rs_ctx *c, long long count, Issue issue, Widen widen, long lon
     }
 }
 
+static void fetch_i64_staged(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind);
+
+static bool page_locked(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 // D2H of `count` int64 values.  kind: 0 = values in [0, 2^32), 1 = values in
 // [-1, 2^31) (sign-extended), 2 = nondecreasing offsets.
+// A page-locked destination lets both limits work at once: the leading part
+// of the array is DMA'd as int64 straight into it on a side stream (PCIe
+// bound) while the rest goes through the wire-word pipeline (bound by the
+// host's memory bandwidth).  RS_DIRECT_FRAC (default 0.5) sets the split.
 void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind) {
     if (count <= 0) return;
+    if ((size_t)count * 8 < kMinStaged) {
+        d2h(c, dst, dsrc, 8 * (size_t)count);
+        RS_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    double frac = 0.5;
+    if (const char *e = std::getenv("RS_DIRECT_FRAC")) frac = std::atof(e);
+    long long direct = 0;
+    if (count >= 4 * kChunk && frac > 0 && page_locked(dst))
+        direct = std::min(count, (long long)(frac * (double)count) & ~1023ll);
+    if (direct > 0) {
+        if (!c->xfer_side) RS_CUDA(cudaStreamCreateWithFlags(&c->xfer_side, cudaStreamNonBlocking));
+        if (!c->xfer_side_ev) RS_CUDA(cudaEventCreateWithFlags(&c->xfer_side_ev, cudaEventDisableTiming));
+        RS_CUDA(cudaEventRecord(c->xfer_side_ev, c->stream));  // after the producing kernels
+        RS_CUDA(cudaStreamWaitEvent(c->xfer_side, c->xfer_side_ev, 0));
+        RS_CUDA(cudaMemcpyAsync(dst, dsrc, 8 * (size_t)direct, cudaMemcpyDeviceToHost, c->xfer_side));
+    }
+    if (count > direct) fetch_i64_staged(c, dst + direct, dsrc + direct, count - direct, kind);
+    if (direct > 0) RS_CUDA(cudaStreamSynchronize(c->xfer_side));
+}
+
+static void fetch_i64_staged(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind) {
     if ((size_t)count * 8 < kMinStaged) {
         d2h(c, dst, dsrc, 8 * (size_t)count);
         RS_CUDA(cudaStreamSynchronize(c->stream));
