@@ -80,12 +80,54 @@ def check(data):
     return None
 
 
+def check_shards(data, world, given_sa):
+    """Query from resident structures by position shards (rs_query_structures_shard,
+    the multi-GPU value path), structures given by the caller (with a consistent
+    or a perturbed sa) or built on device; stitched shards vs the oracle."""
+    from paper_1501_06663_b200 import _native
+    from paper_1501_06663_b200 import distributed as D
+    n = int(data.size)
+    want = oracle.build_suffix_structures(data, workers=8)
+    wl, wo, wf = oracle.all_positions(data, mode="all", structures=want, workers=8)
+    ctx = _native.context()
+    with ctx.lock:
+        if given_sa == "device":
+            ctx.call("rs_set_text", _native.u8(data), n)
+            ctx.call("rs_build_structures")
+        else:
+            sa = want[0].copy()
+            if given_sa == "perturbed" and n > 3:
+                sa[[1, 2]] = sa[[2, 1]]
+            ctx.call("rs_set_structures", _native.i64(sa), _native.i64(want[1]), _native.i64(want[2]), n)
+        L = np.zeros(n + 1, np.int64)
+        O = np.zeros(n + 2, np.int64)
+        flats, base = [], 0
+        for r in range(world):
+            lo, hi = D.shard_range(n, world, r)
+            tot = np.zeros(1, np.int64)
+            ctx.call("rs_query_structures_shard", 1, lo, hi, _native.i64(tot))
+            ctx.call("rs_shard_rebase", base)
+            a = np.zeros(hi - lo, np.int64)
+            b = np.zeros(hi - lo + 1, np.int64)
+            f = np.zeros(int(tot[0]), np.int64)
+            ctx.call("rs_fetch_shard", 1, _native.i64(a), _native.i64(b), _native.i64(f))
+            L[lo:hi] = a
+            O[lo + 1:hi + 1] = b[1:]
+            flats.append(f)
+            base += f.size
+    F = np.concatenate(flats) if flats else np.zeros(0, np.int64)
+    ok = np.array_equal(L, wl) and np.array_equal(O, wo) and np.array_equal(F, wf)
+    return None if ok else f"shards/{world}/{given_sa}"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--seconds", type=float, default=120.0)
     ap.add_argument("--max-n", type=int, default=2_000_000)
     ap.add_argument("--dist", action="store_true", help="the loopback distributed sort with 1..6 ranks")
+    ap.add_argument("--shards", action="store_true",
+                    help="query from resident structures by 1..9 position shards")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t0, cases = time.time(), 0
@@ -96,6 +138,11 @@ def main():
             world = int(rng.integers(1, 7))
             bad, note = check_dist(data, world)
             note = f" world={world} {note}"
+        elif a.shards:
+            world = int(rng.integers(1, 10))
+            how = ("device", "consistent", "perturbed")[int(rng.integers(0, 3))]
+            bad = check_shards(data, world, how)
+            note = f" shards={world} {how}"
         else:
             bad = check(data)
         cases += 1
