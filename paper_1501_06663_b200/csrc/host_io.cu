@@ -55,6 +55,9 @@ class Pool {
             f(0, 1);
             return;
         }
+        // one job at a time: contexts of different devices may transfer from
+        // different host threads concurrently
+        std::lock_guard<std::mutex> one(run_m_);
         {
             std::unique_lock<std::mutex> lk(m_);
             job_ = &f;
@@ -106,6 +109,7 @@ class Pool {
         }
     }
     std::vector<std::thread> workers_;
+    std::mutex run_m_;
     std::mutex m_;
     std::condition_variable cv_, done_;
     const std::function<void(int, int)> *job_ = nullptr;
