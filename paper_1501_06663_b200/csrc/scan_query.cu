@@ -68,11 +68,11 @@ struct CandSoA {
 template <bool RAW>
 __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict__ raw, long long count,
                          long long kb, long long ke, long long tiles, long long *__restrict__ bounds,
-                         long long min_lo, long long tile_positions = kG) {
+                         long long min_lo) {
     long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (g >= tiles) return;
-    long long kfirst = kb + g * tile_positions;
-    long long klast = kfirst + tile_positions - 1;
+    long long kfirst = kb + g * kG;
+    long long klast = kfirst + kG - 1;
     if (klast > ke) klast = ke;
     long long lo, hi;
     if (RAW) {
@@ -564,275 +564,6 @@ __global__ void __launch_bounds__(kNT, 8) k_query_fused(const unsigned *__restri
     query_tile<CandSoA, ALL>(c, x);
 }
 
-// ---------------------------------------------------------------------------
-// Sliding-window sweep (compact path, compaction implicit; the default when
-// every 2048-position tile's raw range fits its stage).
-//
-// The answers at k are the maximum and the argmax set of raw[i] over the
-// window i in [i0(k), k] (i0(k) = first slot whose raw end i + raw[i] - 1
-// reaches k).  Slots the compaction would drop (raw[i] = raw[i-1] - 1) share
-// their end with slot i-1 and are shorter, so they are never a maximum and
-// the argmax set equals Algorithm 4's tie set (_kernels_numba.py:158-195).
-// Both window ends only move right, so each thread sweeps kSPT CONSECUTIVE
-// positions with a monotonic deque (values non-increasing front to back: a
-// slot is dropped only when a later slot -- whose end is no earlier -- is
-// strictly longer): per position one push, amortised O(1) pops, and the ties
-// are exactly the deque's front run of equal values, in start order.  No
-// per-position window walk, no window-bound arrays, no compaction scan.
-// Pass A counts (lengths staged in shared memory), a block scan gives every
-// thread its tile-local tie offset, pass B repeats the sweep and lists the
-// ties in shared memory, warp 0 resolves the tile's CSR base (decoupled
-// look-back, aggregate published before pass B), then everything is stored
-// coalesced.  A thread whose deque would exceed kDQ entries (long windows of
-// decreasing lengths: repetitive text) walks its windows directly instead.
-constexpr int kSNT = 256;
-constexpr int kSPT = 8;
-constexpr int kSG = kSNT * kSPT;              // positions per tile
-constexpr int kSStage = kSG + 768 + 16;       // staged raw slots (incl. alignment and slot lo-1)
-constexpr int kDQ = 8;                        // deque entries per thread
-constexpr int kSTiesCap = kSG * 21 / 8;       // 2.6 ties per position
-constexpr int kSPad = kSNT + 2;               // u16 transposed-staging row (bank spread)
-constexpr int kSRegion1 = ((4 * kSStage + 127) / 128) * 128;  // u32 TMA stage, then s_len + s_off
-static_assert(2 * 2 * kSPT * kSPad <= kSRegion1, "s_len + s_off fit in the dead stage");
-constexpr int kSRaw16 = ((2 * kSStage + 127) / 128) * 128;
-constexpr int kSDeque = 4 * kDQ * kSNT;
-constexpr int kSweepSmem = kSRegion1 + kSRaw16 + kSDeque + 2 * kSTiesCap;
-static_assert(kSStage < 65536 && kSTiesCap < 65536, "u16 slots and tie offsets");
-
-struct Sweep {
-    const unsigned short *r;  // raw values, stage-relative slots
-    unsigned *dq;             // this thread's ring: dq[e * kSNT]
-    long long a;              // global slot of stage slot 0
-    unsigned head, size;      // ring state
-    bool naive;               // deque overflowed: direct window walks
-    unsigned lo_ptr;          // first slot whose end reaches the current position
-    __device__ __forceinline__ unsigned val(unsigned s) const { return r[s]; }
-    // end of stage slot s, as an offset from the stage start (a + s + r - 1 - a)
-    __device__ __forceinline__ int end(unsigned s) const { return (int)s + (int)r[s] - 1; }
-    __device__ __forceinline__ unsigned at(unsigned e) const { return dq[((head + e) % kDQ) * kSNT]; }
-    __device__ __forceinline__ void push(unsigned s) {
-        const unsigned v = r[s];
-        if (v == 0 || naive) return;
-        while (size && (at(size - 1) & 0xffffu) < v) --size;
-        if (size == kDQ) {
-            naive = true;
-            return;
-        }
-        dq[((head + size) % kDQ) * kSNT] = (s << 16) | v;
-        ++size;
-    }
-    // move to position k (stage-relative kr): push slot kr, expire the front,
-    // advance lo_ptr; returns the maximum (0: no repeat covers k)
-    __device__ __forceinline__ unsigned step(int kr) {
-        push((unsigned)kr);
-        while ((int)lo_ptr <= kr && end(lo_ptr) < kr) ++lo_ptr;
-        if (naive) {
-            unsigned m = 0;
-            for (int s = (int)lo_ptr; s <= kr; ++s) m = max(m, val((unsigned)s));
-            return m;
-        }
-        while (size && end(at(0) >> 16) < kr) {
-            head = (head + 1) % kDQ;
-            --size;
-        }
-        return size ? (at(0) & 0xffffu) : 0u;
-    }
-};
-
-template <bool ALL>
-__global__ void __launch_bounds__(kSNT) k_query_sweep(const unsigned *__restrict__ raw, long long kb, long long ke,
-                                                     const long long *__restrict__ bounds, int out_off,
-                                                     long long *__restrict__ out0, long long *__restrict__ out1,
-                                                     long long *__restrict__ flat, long long flat_cap, u64 *status,
-                                                     long long tiles, unsigned long long *total_out,
-                                                     unsigned ties_cap) {
-    extern __shared__ __align__(128) unsigned char dsm[];
-    unsigned *s_stage = reinterpret_cast<unsigned *>(dsm);
-    unsigned short *s_len = reinterpret_cast<unsigned short *>(dsm);      // after the u16 copy
-    unsigned short *s_off = s_len + kSPT * kSPad;
-    unsigned short *s_r = reinterpret_cast<unsigned short *>(dsm + kSRegion1);
-    unsigned *s_dq = reinterpret_cast<unsigned *>(dsm + kSRegion1 + kSRaw16);
-    unsigned short *s_ties = reinterpret_cast<unsigned short *>(dsm + kSRegion1 + kSRaw16 + kSDeque);
-    __shared__ __align__(8) unsigned long long s_bar;
-    __shared__ unsigned s_warp[kSNT / 32];
-    __shared__ u64 s_base;
-
-    const long long tile = blockIdx.x;  // dispatch-order assumption: see lookback_warp
-    const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];  // raw slots [lo, hi)
-    const long long tile_k0 = kb + tile * kSG;
-    const int npos = (int)((ke - tile_k0 + 1) < kSG ? (ke - tile_k0 + 1) : kSG);
-    const long long slot0 = tile_k0 - kb + out_off;
-    const long long a = (lo - 1) & ~3ll, b = (hi + 3) & ~3ll;  // stage raw[a, b), 16-byte aligned
-    const int nst = (int)(b - a);
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        const unsigned bytes = (unsigned)(nst * 4);
-        mbar_expect_tx(&s_bar, bytes);
-        tma_load_1d(s_stage, raw + a, bytes, &s_bar);
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-    for (int i = threadIdx.x; i < nst; i += kSNT) s_r[i] = (unsigned short)s_stage[i];
-    __syncthreads();  // the u32 stage is dead: s_len / s_off take its place
-
-    const int p0 = threadIdx.x * kSPT;           // tile-local first position of this thread
-    const int k0r = (int)(tile_k0 + p0 - a);     // its stage-relative slot
-    const int lo_r = (int)(lo - a);
-    Sweep sw;
-    sw.r = s_r;
-    sw.dq = s_dq + threadIdx.x;
-    sw.a = a;
-    auto start = [&]() {  // window of the thread's first position, minus slot k0 itself
-        sw.head = sw.size = 0;
-        sw.naive = false;
-        int x = lo_r, y = k0r;  // first slot s in [lo_r, k0r) with end(s) >= k0r, else k0r
-        while (x < y) {
-            const int mid = (x + y) >> 1;
-            if (sw.end((unsigned)mid) >= k0r) y = mid; else x = mid + 1;
-        }
-        sw.lo_ptr = (unsigned)x;
-        for (int s = x; s < k0r; ++s) sw.push((unsigned)s);
-    };
-    const int mine = npos - p0 < kSPT ? (npos - p0 > 0 ? npos - p0 : 0) : kSPT;
-
-    // ---- pass A: maxima and tie counts ----
-    unsigned cnt_pack[kSPT / 2];
-#pragma unroll
-    for (int j = 0; j < kSPT / 2; ++j) cnt_pack[j] = 0;
-    unsigned total = 0;
-    if (mine > 0) {
-        start();
-#pragma unroll
-        for (int j = 0; j < kSPT; ++j) {
-            if (j >= mine) break;
-            const int kr = k0r + j;
-            const unsigned M = sw.step(kr);
-            unsigned nt = 0;
-            if (M) {
-                if (!sw.naive) {
-                    while (nt < sw.size && (sw.at(nt) & 0xffffu) == M) ++nt;
-                } else {
-                    for (int s = (int)sw.lo_ptr; s <= kr; ++s) nt += sw.val((unsigned)s) == M;
-                }
-            }
-            if (ALL) {
-                s_len[j * kSPad + threadIdx.x] = (unsigned short)M;
-                cnt_pack[j >> 1] |= nt << (16 * (j & 1));
-                total += nt;
-            } else {
-                unsigned first = 0;
-                if (M) {
-                    if (!sw.naive) {
-                        first = sw.at(0) >> 16;
-                    } else {
-                        int s = (int)sw.lo_ptr;
-                        while (sw.val((unsigned)s) != M) ++s;
-                        first = (unsigned)s;
-                    }
-                }
-                out0[slot0 + p0 + j] = M ? a + (long long)first : -1ll;
-                out1[slot0 + p0 + j] = M;
-            }
-        }
-    }
-    if (!ALL) {
-        if (tile == 0 && threadIdx.x == 0 && out_off) {
-            out0[0] = -1;
-            out1[0] = 0;
-        }
-        return;
-    }
-#define RS_SNT(j) ((cnt_pack[(j) >> 1] >> (16 * ((j) & 1))) & 0xffffu)
-
-    // ---- tile-local offsets (block scan), aggregate published at once ----
-    unsigned excl;
-    const unsigned block_total = block_exclusive_sum<kSNT, false>(total, excl, s_warp);
-    if (threadIdx.x == 0) lookback_publish(status, tile, (u64)block_total);
-    {
-        unsigned acc = excl;
-#pragma unroll
-        for (int j = 0; j < kSPT; ++j) {
-            acc += RS_SNT(j);
-            s_off[j * kSPad + threadIdx.x] = (unsigned short)acc;  // inclusive, tile-local
-        }
-    }
-    const bool staged = block_total <= ties_cap;
-
-    // ---- pass B: the same sweep, ties listed in shared memory ----
-    if (staged && mine > 0 && total > 0) {
-        start();
-        unsigned w = excl;
-#pragma unroll
-        for (int j = 0; j < kSPT; ++j) {
-            if (j >= mine) break;
-            const int kr = k0r + j;
-            const unsigned M = sw.step(kr);
-            if (!M) continue;
-            if (!sw.naive) {
-                for (unsigned e = 0; e < sw.size; ++e) {
-                    const unsigned q = sw.at(e);
-                    if ((q & 0xffffu) != M) break;
-                    s_ties[w++] = (unsigned short)(q >> 16);
-                }
-            } else {
-                for (int s = (int)sw.lo_ptr; s <= kr; ++s)
-                    if (sw.val((unsigned)s) == M) s_ties[w++] = (unsigned short)s;
-            }
-        }
-    }
-    if (threadIdx.x < 32) {
-        const u64 base = lookback_warp(status, tile, (u64)block_total, OpSum(), true);
-        if (threadIdx.x == 0) {
-            s_base = base;
-            if (tile == tiles - 1) *total_out = base + block_total;
-        }
-    }
-    __syncthreads();
-    const u64 tile_base = s_base;
-    if (tile == 0 && threadIdx.x == 0) {
-        if (out_off) {
-            out0[0] = 0;  // lengths[0]
-            out1[0] = 0;  // offsets[0]
-        }
-        out1[out_off] = 0;  // offsets of the first position
-    }
-    for (int p = threadIdx.x; p < npos; p += kSNT) {  // p = t * kSPT + j  ->  row j, column t
-        const int idx = (p % kSPT) * kSPad + p / kSPT;
-        out0[slot0 + p] = s_len[idx];
-        out1[slot0 + 1 + p] = (long long)(tile_base + s_off[idx]);
-    }
-    if (staged && (long long)(tile_base + block_total) <= flat_cap) {
-        long long *const ft = flat + tile_base;
-        for (unsigned i = threadIdx.x; i < block_total; i += kSNT) ft[i] = a + (long long)s_ties[i];
-        return;
-    }
-    // direct stores (tie list overflow, or flat capacity exceeded: the host re-runs)
-    if (mine > 0 && total > 0) {
-        start();
-        long long w = (long long)(tile_base + excl);
-        for (int j = 0; j < mine; ++j) {
-            const int kr = k0r + j;
-            const unsigned M = sw.step(kr);
-            if (!M) continue;
-            if (!sw.naive) {
-                for (unsigned e = 0; e < sw.size; ++e) {
-                    const unsigned q = sw.at(e);
-                    if ((q & 0xffffu) != M) break;
-                    if (w < flat_cap) flat[w] = a + (long long)(q >> 16);
-                    ++w;
-                }
-            } else {
-                for (int s = (int)sw.lo_ptr; s <= kr; ++s)
-                    if (sw.val((unsigned)s) == M) {
-                        if (w < flat_cap) flat[w] = a + (long long)s;
-                        ++w;
-                    }
-            }
-        }
-    }
-#undef RS_SNT
-}
-
 // max over tiles of the staged raw range (hi - lo + 8) -> *out
 __global__ void k_max_span(const long long *__restrict__ bounds, long long tiles, unsigned long long *out) {
     long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -950,66 +681,6 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
     const bool rawp = path == RS_PATH_RAW;
     long long npos = ke - kb + 1;
     if (npos <= 0) return true;
-    // compact path without LLRc: the sliding-window sweep over 2048-position
-    // tiles when every tile's raw range fits its stage (RS_SCAN=walk: the
-    // per-position window walk of k_query_fused, for A/B runs)
-    bool sweep = false;
-    if (fused) {
-        const char *scan_env = std::getenv("RS_SCAN");
-        if (!(scan_env && std::strcmp(scan_env, "walk") == 0)) {
-            const long long st = (npos + kSG - 1) / kSG;
-            long long *sb = (long long *)buf(c, B_BOUNDS, sizeof(long long) * 2 * (size_t)st);
-            RS_LAUNCH(c, k_bounds<true>, grid_for(st, 128), 128, 0, d_e, d_raw, count, kb, ke, st, sb, min_lo,
-                      (long long)kSG);
-            unsigned long long *span = (unsigned long long *)buf(c, B_SMALL, 4096) + 6;
-            RS_CUDA(cudaMemsetAsync(span, 0, sizeof(*span), c->stream));
-            RS_LAUNCH(c, k_max_span, grid_for(st, 256), 256, 0, sb, st, span);
-            unsigned long long mx = 0;
-            fetch_small(c, &mx, span, sizeof(mx));
-            sweep = mx <= (unsigned long long)kSStage;
-        }
-    }
-    if (sweep) {
-        static unsigned long long sattr = 0;
-        once_per_device(sattr, c->device, [] {
-            RS_CUDA(cudaFuncSetAttribute(k_query_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
-            RS_CUDA(cudaFuncSetAttribute(k_query_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
-        });
-        const long long st = (npos + kSG - 1) / kSG;
-        const long long *sb = (const long long *)c->bufs[B_BOUNDS].p;
-        long long *out0 = (long long *)buf(c, B_OUT0, sizeof(long long) * (size_t)(n_slots + 1));
-        long long *out1 = (long long *)buf(c, B_OUT1, sizeof(long long) * (size_t)(n_slots + 2));
-        unsigned long long *tot = (unsigned long long *)buf(c, B_SMALL, 4096) + 2;
-        const double qbytes = 4.0 * (double)npos + 16.0 * (double)npos;
-        if (!all) {
-            RS_LAUNCH_B(c, qbytes, (k_query_sweep<false>), (unsigned)st, kSNT, kSweepSmem, d_raw, kb, ke, sb, out_off,
-                        out0, out1, nullptr, 0, nullptr, st, tot, 0u);
-            c->out_mode = 0;
-            return true;
-        }
-        size_t cap_slots = c->bufs[B_FLAT].cap / sizeof(long long);
-        size_t want = (size_t)(2 * npos + 64);
-        if (cap_slots < want) cap_slots = want;
-        for (int attempt = 0; attempt < 3; ++attempt) {
-            long long *flat = (long long *)buf(c, B_FLAT, sizeof(long long) * cap_slots);
-            Scratch scr = scratch(c, st);
-            unsigned ties_cap = kSTiesCap;
-            if (const char *e = std::getenv("RS_FUSED_TIES_CAP")) {  // tests: exercise the direct stores
-                const long v = std::strtol(e, nullptr, 10);
-                if (v >= 0 && v < ties_cap) ties_cap = (unsigned)v;
-            }
-            RS_LAUNCH_B(c, qbytes, (k_query_sweep<true>), (unsigned)st, kSNT, kSweepSmem, d_raw, kb, ke, sb, out_off,
-                        out0, out1, flat, (long long)cap_slots, scr.status, st, tot, ties_cap);
-            unsigned long long T = 0;
-            fetch_small(c, &T, tot, sizeof(T));
-            add_bytes_last(c, 8.0 * (double)T);
-            c->total = (long long)T;
-            c->out_mode = 1;
-            if ((size_t)T <= cap_slots) return true;
-            cap_slots = (size_t)T + 64;
-        }
-        fail(RS_ECUDA, "tie buffer sizing did not converge");
-    }
     long long tiles = (npos + kG - 1) / kG;
     long long *bounds = (long long *)buf(c, B_BOUNDS, sizeof(long long) * 2 * (size_t)tiles);
     if (rawp || fused)
