@@ -169,45 +169,91 @@ def fill_pads(views: dict, mode: str) -> None:
         views["offsets"][1] = 0
 
 
+class _SharedBlock:
+    """One /dev/shm file mapped in this process."""
+    __slots__ = ("path", "nbytes", "mm", "__weakref__")
+
+    def __init__(self, path: str, nbytes: int):
+        import mmap
+        fd = os.open(path, os.O_RDWR)
+        try:
+            self.mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+        finally:
+            os.close(fd)
+        self.path, self.nbytes = path, nbytes
+
+
+_shared_maps: dict[str, _SharedBlock] = {}   # every rank: path -> mapping
+_shared_free: list[tuple[str, int]] = []      # rank 0: blocks whose answers were released
+_shared_files: list[str] = []                 # rank 0: files to remove at exit
+
+
+def _remove_shared_files():
+    for path in _shared_files:
+        try:
+            os.unlink(path)
+        except OSError:
+            pass
+
+
 class SharedHostBuffer:
-    """One int64 host buffer mapped by every rank of the node (/dev/shm file,
-    unlinked as soon as every rank has mapped it).  Raises MemoryError when
-    /dev/shm cannot hold it (callers fall back to the NCCL gather)."""
+    """One int64 host buffer mapped by every rank of the node (a /dev/shm
+    file).  Blocks are cached like the library's host pools: when the arrays
+    rank 0 handed out are released, the block (already page-faulted on every
+    rank) serves the next call -- fresh tmpfs pages cost far more to fault in
+    than the transfer itself.  Raises MemoryError when /dev/shm cannot hold a
+    new block (callers fall back to the NCCL gather)."""
 
     def __init__(self, nelems: int, group=None, root: str = "/dev/shm"):
-        import mmap
+        import atexit
         import uuid
 
         import torch.distributed as dist
         rank = dist.get_rank(group)
-        nbytes = max(8 * int(nelems), 8)
-        name = [None, None]
+        need = max(8 * int(nelems), 8)
+        name = [None, 0, None]
         if rank == 0:
-            try:
-                st = os.statvfs(root)
-                free = st.f_bavail * st.f_frsize
-            except OSError:
-                free = 0
-            if free >= nbytes + (64 << 20):
-                path = os.path.join(root, f"repeatscan_{os.getpid()}_{uuid.uuid4().hex[:12]}")
-                fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
-                os.ftruncate(fd, nbytes)
-                os.close(fd)
-                name = [path, None]
+            fit = [blk for blk in _shared_free if blk[1] >= need]
+            if fit:
+                blk = min(fit, key=lambda b_: b_[1])
+                _shared_free.remove(blk)
+                name = [blk[0], blk[1], None]
             else:
-                name = [None, f"{root} has {free} bytes free, {nbytes} needed"]
+                nbytes = 1 << 20
+                while nbytes < need:
+                    nbytes <<= 1
+                try:
+                    st = os.statvfs(root)
+                    free = st.f_bavail * st.f_frsize
+                except OSError:
+                    free = 0
+                if free >= nbytes + (64 << 20):
+                    path = os.path.join(root, f"repeatscan_{os.getpid()}_{uuid.uuid4().hex[:12]}")
+                    fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+                    os.ftruncate(fd, nbytes)
+                    os.close(fd)
+                    if not _shared_files:
+                        atexit.register(_remove_shared_files)
+                    _shared_files.append(path)
+                    name = [path, nbytes, None]
+                else:
+                    name = [None, 0, f"{root} has {free} bytes free, {nbytes} needed"]
         dist.broadcast_object_list(name, src=0, group=group)
         if name[0] is None:
-            raise MemoryError(name[1])
-        fd = os.open(name[0], os.O_RDWR)
-        try:
-            self._mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
-        finally:
-            os.close(fd)
+            raise MemoryError(name[2])
+        blk = _shared_maps.get(name[0])
+        if blk is None or blk.nbytes != name[1]:
+            blk = _SharedBlock(name[0], int(name[1]))
+            _shared_maps[name[0]] = blk
         dist.barrier(group=group)
+        # owner of the returned arrays: the block goes back to rank 0's free
+        # list when the last view of them dies
+        import ctypes as _ct
+        import weakref
+        raw = (_ct.c_char * blk.nbytes).from_buffer(blk.mm)
         if rank == 0:
-            os.unlink(name[0])
-        self.array = np.frombuffer(self._mm, dtype=np.int64, count=int(nelems))
+            weakref.finalize(raw, _shared_free.append, (blk.path, blk.nbytes))
+        self.array = np.frombuffer(raw, dtype=np.int64, count=int(nelems))
 
 
 def fetch_shard_shared(ctx, n: int, mode: str, lo: int, hi: int, base: int, totals: list[int],
