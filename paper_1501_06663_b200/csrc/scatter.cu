@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(kApplyNT) k_bucket_apply(const uint2 *__restri
 constexpr int kRNT = 256;
 constexpr int kRIPT = 8;
 __global__ void __launch_bounds__(kRNT) k_raw_sa_emit(const unsigned *__restrict__ sa, const unsigned *__restrict__ lcp_d,
-                                                     long long n, BucketEmit be) {
+                                                     long long n, BucketEmit be, unsigned dlo = 0,
+                                                     unsigned dhi = 0xffffffffu) {
     __shared__ EmitSmem<kRNT, kRIPT> sm;
     const long long r0 = (blockIdx.x * (long long)kRNT + threadIdx.x) * kRIPT;
     unsigned dest[kRIPT], val[kRIPT];
@@ -88,6 +89,11 @@ __global__ void __launch_bounds__(kRNT) k_raw_sa_emit(const unsigned *__restrict
                 dest[j] = 0xffffffffu;
             }
         }
+    }
+    if (dlo != 0 || dhi != 0xffffffffu) {  // a position shard: only slots [dlo, dhi]
+#pragma unroll
+        for (int j = 0; j < kRIPT; ++j)
+            if (dest[j] < dlo || dest[j] > dhi) dest[j] = 0xffffffffu;
     }
     bucket_emit<kRNT, kRIPT>(be, dest, val, sm);
 }
@@ -221,6 +227,18 @@ void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n) {
     RS_LAUNCH_B(c, 16.0 * n, k_raw_sa_emit, grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0,
                 (const unsigned *)c->bufs[B_SA].p, (const unsigned *)c->bufs[B_LCP].p, n, be);
     bucket_apply(c, be, raw, n);
+}
+
+// raw slots [first, last] only (a position shard + its halo), SA order: every
+// rank reads the whole SA / LCP once but emits and scatters only its slots
+void raw_from_sa_lcp_range(rs_ctx *c, long long n, size_t raw_slots_n, long long first, long long last) {
+    unsigned *raw = (unsigned *)buf(c, B_RAW, sizeof(unsigned) * raw_slots_n);
+    RS_CUDA(cudaMemsetAsync(raw, 0, sizeof(unsigned), c->stream));
+    BucketEmit be = bucket_setup(c, n + 1, 0);
+    RS_LAUNCH_B(c, 8.0 * n + 8.0 * (double)(last - first + 1), k_raw_sa_emit,
+                grid_for((n + kRIPT - 1) / kRIPT, kRNT), kRNT, 0, (const unsigned *)c->bufs[B_SA].p,
+                (const unsigned *)c->bufs[B_LCP].p, n, be, (unsigned)first, (unsigned)last);
+    bucket_apply(c, be, raw, last - first + 1);
 }
 
 void scatter_phi(rs_ctx *c, const unsigned *sa, long long n, unsigned *phi) {

@@ -96,6 +96,7 @@ BucketEmit bucket_setup(rs_ctx *c, long long n_out, int slot = 0, bool two = fal
 void bucket_apply(rs_ctx *c, const BucketEmit &be, unsigned *out, long long elems, unsigned *out2 = nullptr,
                   int out2_shift = 0);
 void raw_from_sa_lcp(rs_ctx *c, long long n, size_t raw_slots_n);
+void raw_from_sa_lcp_range(rs_ctx *c, long long n, size_t raw_slots_n, long long first, long long last);
 // phi[sa[j]] = sa[j-1] (0xffffffff at j = 0) through the bucketed scatter.
 void scatter_phi(rs_ctx *c, const unsigned *sa, long long n, unsigned *phi);
 // isa[sa[r]] = r through the bucketed scatter.
