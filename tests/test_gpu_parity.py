@@ -654,3 +654,21 @@ def test_structures_shards_assemble_to_full_answer(structures_from):
             assert np.array_equal(offsets, want_o), world
             assert np.array_equal(np.concatenate(flats), want_f), world
             assert np.array_equal(starts, want_s) and np.array_equal(llen, want_len), world
+
+
+@pytest.mark.parametrize("n", [(1 << 20) - 1, (1 << 24) + 1])
+def test_transfer_pipeline_boundaries(n):
+    """Answers that cross the staging threshold (2^20 values) and the
+    pipeline's 2^24-value chunks, fetched into pageable (pipeline only) and
+    page-locked (30% direct DMA + pipeline) arrays: identical, and correct by
+    the independent checker (count_wrong_answers)."""
+    from paper_1501_06663_b200.query import count_wrong_answers
+    data = workloads.iid_dna(n, 77)
+    t = rb.Text(data)
+    A = rb.all_positions(t, mode="all")
+    P = rb.all_positions(t, mode="all", pinned=True)
+    assert np.array_equal(A.lengths, P.lengths) and np.array_equal(A.offsets, P.offsets)
+    assert np.array_equal(A.flat_starts, P.flat_starts)
+    L = rb.all_positions(t, mode="leftmost", pinned=True)
+    c = rb.build_compact_llr(rb.build_raw_llr(rb.build_suffix_structures(t)))
+    assert count_wrong_answers(c, n, all_answers=A, leftmost=L) == 0
