@@ -144,7 +144,9 @@ __global__ void k_make_keys(const unsigned *__restrict__ G, const unsigned *__re
 
 // Dense ordinal of each list entry's group (runs of equal heads): exclusive
 // count of run starts, block scan + decoupled look-back; total -> *groups.
-constexpr int kGNT = 256, kGIPT = 8, kGTile = kGNT * kGIPT;
+// 32 entries per thread: one look-back per 8192 entries (8 per thread left the
+// tiles waiting on their predecessors)
+constexpr int kGNT = 256, kGIPT = 32, kGTile = kGNT * kGIPT;
 __global__ void __launch_bounds__(kGNT) k_group_ordinals(const unsigned *__restrict__ H, long long U,
                                                        unsigned *__restrict__ G, unsigned long long *groups,
                                                        unsigned *counter, u64 *status, long long tiles) {
@@ -159,11 +161,13 @@ __global__ void __launch_bounds__(kGNT) k_group_ordinals(const unsigned *__restr
     unsigned prev = (t0 > 0 && t0 - 1 < U) ? H[t0 - 1] : 0xffffffffu;
     unsigned hv[kGIPT];
     const bool full = t0 + kGIPT <= U;
-    if (full) {  // two 16-byte loads
+    if (full) {  // 16-byte loads
         const uint4 *q = reinterpret_cast<const uint4 *>(H + t0);
-        const uint4 a = q[0], b = q[1];
-        hv[0] = a.x; hv[1] = a.y; hv[2] = a.z; hv[3] = a.w;
-        hv[4] = b.x; hv[5] = b.y; hv[6] = b.z; hv[7] = b.w;
+#pragma unroll
+        for (int w = 0; w < kGIPT / 4; ++w) {
+            const uint4 a = q[w];
+            hv[4 * w] = a.x; hv[4 * w + 1] = a.y; hv[4 * w + 2] = a.z; hv[4 * w + 3] = a.w;
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < kGIPT; ++j) hv[j] = t0 + j < U ? H[t0 + j] : 0u;
@@ -197,8 +201,8 @@ __global__ void __launch_bounds__(kGNT) k_group_ordinals(const unsigned *__restr
     }
     if (full) {
         uint4 *q = reinterpret_cast<uint4 *>(G + t0);
-        q[0] = make_uint4(gv[0], gv[1], gv[2], gv[3]);
-        q[1] = make_uint4(gv[4], gv[5], gv[6], gv[7]);
+#pragma unroll
+        for (int w = 0; w < kGIPT / 4; ++w) q[w] = make_uint4(gv[4 * w], gv[4 * w + 1], gv[4 * w + 2], gv[4 * w + 3]);
     } else {
 #pragma unroll
         for (int j = 0; j < kGIPT; ++j)
