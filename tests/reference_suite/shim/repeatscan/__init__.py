@@ -21,3 +21,13 @@ _MODULES = {
 
 for _alias, _real in _MODULES.items():
     sys.modules[_alias] = importlib.import_module(_real)
+
+# CUDA context creation (driver init, module load) happens once per process,
+# here at import -- the reference's counterpart is numba's JIT warm-up, which
+# its acceptance tests do before timing (test_acceptance.py:238); without it
+# the first timed call of the suite (criterion 1: < 1 s) pays the driver start.
+try:
+    from paper_1501_06663_b200 import _native as _n
+    _n.context()
+except Exception:  # no device: the suite's own calls raise the real error
+    pass
