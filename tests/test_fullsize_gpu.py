@@ -127,3 +127,20 @@ def test_answer_checker_detects_faults(rng):
         s2 = starts.copy()
         s2[k] = flat[o + 1]
         assert count_wrong_answers(c, n, leftmost=rb.LeftmostAnswers(s2, llen)) == 1
+
+
+@pytest.mark.parametrize("config", ["C2", "C3", "C4"])
+def test_full_size_raw_path_digests(config):
+    """The raw path (Algorithms 1/3 over the raw LLR array, k_query<raw>) at
+    full size gives the same committed digests (raw and compact
+    answers are identical).  C5 is skipped: its raw walk is ~alpha*n =
+    ~10^13 steps (the reference restricts it to the compact path too)."""
+    rec = _rec(config)
+    t = rb.Text(workloads.make(config))
+    A = rb.all_positions(t, mode="all", path="raw")
+    assert A.flat_starts.size == rec["T"]
+    assert dg(A.lengths) == rec["a_lengths"] and dg(A.offsets) == rec["a_offsets"]
+    assert dg(A.flat_starts) == rec["a_flat"]
+    del A
+    L = rb.all_positions(t, mode="leftmost", path="raw")
+    assert dg(L.starts) == rec["l_starts"] and dg(L.lengths) == rec["l_lengths"]

@@ -672,3 +672,41 @@ def test_transfer_pipeline_boundaries(n):
     L = rb.all_positions(t, mode="leftmost", pinned=True)
     c = rb.build_compact_llr(rb.build_raw_llr(rb.build_suffix_structures(t)))
     assert count_wrong_answers(c, n, all_answers=A, leftmost=L) == 0
+
+
+def test_new_entry_points_errors():
+    """Status codes of the round-2 entry points map to the reference's
+    exception types (_native._raise): bad order -> RepeatscanError(ESTATE),
+    bad ranges -> IndexError, bad arguments -> ValueError."""
+    from paper_1501_06663_b200 import _native
+    ctx = _native.Context(0)  # a fresh context: nothing loaded, no communicator
+    try:
+        tot = np.zeros(1, np.int64)
+        with pytest.raises(_native.RepeatscanError):
+            ctx.call("rs_query_structures_shard", 1, 1, 2, _native.i64(tot))
+        with pytest.raises(_native.RepeatscanError):
+            ctx.call("rs_clear_llr")
+        with pytest.raises(_native.RepeatscanError):
+            ctx.call("rs_nccl_allgather_i64", 1, _native.i64(tot))
+        data = workloads.iid_dna(1000, 3)
+        ctx.call("rs_set_text", _native.u8(data), data.size)
+        ctx.call("rs_build_structures")
+        with pytest.raises(IndexError):
+            ctx.call("rs_query_structures_shard", 1, 0, 5, _native.i64(tot))
+        with pytest.raises(IndexError):
+            ctx.call("rs_query_structures_shard", 1, 10, 2000, _native.i64(tot))
+        with pytest.raises(ValueError):
+            ctx.call("rs_query_structures_shard", 7, 1, 5, _native.i64(tot))
+        ctx.call("rs_query_structures_shard", 1, 5, 5, _native.i64(tot))  # empty shard
+        assert tot[0] == 0
+        bad = np.zeros(1, np.int64)
+        with pytest.raises(ValueError):  # m > n
+            ctx.call("rs_check_answers", _native.i64(bad), _native.i64(bad), 5, 1, None, None, None, 0,
+                     None, None, _native.i64(bad))
+        s = rb.build_suffix_structures(rb.Text(data))
+        rank = s.rank.copy()
+        rank[3] = 0  # out of 1..n
+        with pytest.raises(ValueError):
+            ctx.call("rs_set_structures", _native.i64(s.sa), _native.i64(rank), _native.i64(s.lcp), data.size)
+    finally:
+        ctx.close()
