@@ -161,6 +161,19 @@ def _shared_worker(rank, world, port, data, q):
             dist.barrier()
             out[mode] = {k: v.copy() for k, v in views.items()}
             dist.barrier()
+        # a released block is reused by the next call of the same size (warm pages)
+        sizes = sum(c for _, c in D.answer_layout(n, "all", sum(totals)).values())
+        b1 = D.SharedHostBuffer(sizes)
+        p1 = b1.array.ctypes.data
+        del b1
+        import gc
+        gc.collect()
+        dist.barrier()
+        b2 = D.SharedHostBuffer(sizes)
+        reused = b2.array.ctypes.data == p1
+        if rank == 0:
+            assert reused, "released shared block not reused"
+        del b2
         if rank == 0:
             A, L = out["all"], out["leftmost"]
             ok = (np.array_equal(A["lengths"], wl) and np.array_equal(A["offsets"], wo)
