@@ -22,7 +22,7 @@ NVCC_FLAGS = [
 
 
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def needs_build() -> bool:

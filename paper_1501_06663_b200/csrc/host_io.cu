@@ -32,6 +32,10 @@
 
 namespace rsb {
 
+// host_widen.cpp: out[j] = f(w[j]) + add, streaming stores
+void widen_words(const unsigned *w, long long *out, long long x, long long y, int mode, unsigned w0,
+                 long long add);
+
 namespace {
 
 void h2d(rs_ctx *c, void *dst, const void *src, size_t bytes) {
@@ -269,15 +273,8 @@ static void fetch_i64_staged(rs_ctx *c, long long *dst, const long long *dsrc, l
             return (const void *)d;
         },
         [&](const unsigned *w, long long *out, long long x, long long y, long long chunk) {
-            if (kind == 0) {
-                for (long long j = x; j < y; ++j) out[j] = (long long)w[j];
-            } else if (kind == 1) {
-                for (long long j = x; j < y; ++j) out[j] = (long long)(int)w[j];
-            } else {
-                const long long first = ends_p[2 * chunk];
-                const unsigned w0 = w[0];
-                for (long long j = x; j < y; ++j) out[j] = first + (long long)(unsigned)(w[j] - w0);
-            }
+            if (kind == 2) widen_words(w, out, x, y, 2, w[0], ends_p[2 * chunk]);
+            else widen_words(w, out, x, y, kind, 0u, 0ll);
         },
         dst);
 }
@@ -289,7 +286,7 @@ void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long
     pipeline_out(
         c, count, [&](long long a, long long, int) { return (const void *)(dsrc + a); },
         [&](const unsigned *w, long long *out, long long x, long long y, long long) {
-            for (long long j = x; j < y; ++j) out[j] = (long long)w[j] + add;
+            widen_words(w, out, x, y, 0, 0u, add);
         },
         dst);
 }
