@@ -218,7 +218,7 @@ static bool page_locked(const void *p) {
 // A page-locked destination lets both limits work at once: the leading part
 // of the array is DMA'd as int64 straight into it on a side stream (PCIe
 // bound) while the rest goes through the wire-word pipeline (bound by the
-// host's memory bandwidth).  RS_DIRECT_FRAC (default 0.3) sets the split.
+// host's memory bandwidth).  RS_DIRECT_FRAC (default 0: with streaming stores the pipeline alone is as fast, tools/exp_fetch.py) sets the split.
 void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind) {
     if (count <= 0) return;
     if ((size_t)count * 8 < kMinStaged) {
@@ -226,7 +226,7 @@ void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count
         RS_CUDA(cudaStreamSynchronize(c->stream));
         return;
     }
-    double frac = 0.3;
+    double frac = 0.0;
     if (const char *e = std::getenv("RS_DIRECT_FRAC")) frac = std::atof(e);
     long long direct = 0;
     if (count >= 4 * kChunk && frac > 0 && page_locked(dst))
