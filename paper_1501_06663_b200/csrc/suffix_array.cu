@@ -128,6 +128,11 @@ __global__ void k_pack_text(const unsigned char *__restrict__ text, long long n,
 // group << lo_bits | lo, the group given either as its head slot or as its
 // dense ordinal (the list is in slot order, so groups are consecutive runs
 // of equal heads); both orders agree.
+// During the doubling rounds the ISA entry of a suffix whose group is still
+// tied carries this flag over its group head (slots are < 2^31); sorted
+// suffixes hold their final slot.  Lets the round keys be built in text order.
+constexpr unsigned kUnsortedBit = 0x80000000u;
+
 __global__ void k_make_keys(const unsigned *__restrict__ G, const unsigned *__restrict__ V, long long U,
                             const unsigned *__restrict__ isa, long long n, long long h, int lo_bits,
                             u64 *__restrict__ keys, unsigned *__restrict__ vals) {
@@ -137,9 +142,56 @@ __global__ void k_make_keys(const unsigned *__restrict__ G, const unsigned *__re
     // Suffixes shorter than h (padded with the smallest code) order by length
     // before every longer member of their group: lo = remaining length in
     // [1, h]; otherwise h + 1 + rank of suffix i + h.
-    u64 lo = ((long long)i + h < n) ? (u64)(h + 1) + isa[i + h] : (u64)(n - i);
+    u64 lo = ((long long)i + h < n) ? (u64)(h + 1) + (isa[i + h] & ~kUnsortedBit) : (u64)(n - i);
     keys[t] = ((u64)G[t] << lo_bits) | lo;
     vals[t] = i;
+}
+
+// The same round keys built in TEXT order (large rounds: repetitive text keeps
+// most suffixes tied for many rounds).  isa[i] (the group head, flagged while
+// tied) and isa[i + h] are both read coalesced -- the list version gathers
+// isa[i + h] at random, ~136 B of DRAM per 4-byte key on a 1 GiB text.  The
+// tied suffixes are appended in any order (warp-aggregated counter): the sort
+// orders them by (head, lo), and suffixes with equal keys stay tied.
+constexpr int kMKNT = 256, kMKIPT = 4, kMKTile = kMKNT * kMKIPT;
+__global__ void __launch_bounds__(kMKNT) k_make_keys_text(const unsigned *__restrict__ isa, long long n, long long h,
+                                                        int lo_bits, u64 *__restrict__ keys,
+                                                        unsigned *__restrict__ vals,
+                                                        unsigned long long *__restrict__ counter) {
+    __shared__ u64 s_key[kMKTile];
+    __shared__ unsigned s_val[kMKTile];
+    __shared__ unsigned s_warp[kMKNT / 32];
+    __shared__ unsigned long long s_base;
+    const long long i0 = (blockIdx.x * (long long)kMKNT + threadIdx.x) * kMKIPT;
+    unsigned hd[kMKIPT];
+    if (i0 + kMKIPT <= n) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(isa + i0);
+        hd[0] = q.x, hd[1] = q.y, hd[2] = q.z, hd[3] = q.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kMKIPT; ++j) hd[j] = (i0 + j < n) ? isa[i0 + j] : 0u;
+    }
+    unsigned cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kMKIPT; ++j) cnt += hd[j] >> 31;
+    unsigned excl;
+    const unsigned total = block_exclusive_sum<kMKNT>(cnt, excl, s_warp);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(counter, (unsigned long long)total) : 0;
+#pragma unroll
+    for (int j = 0; j < kMKIPT; ++j) {
+        if (!(hd[j] & kUnsortedBit)) continue;
+        const long long i = i0 + j;
+        const u64 lo = (i + h < n) ? (u64)(h + 1) + (isa[i + h] & ~kUnsortedBit) : (u64)(n - i);
+        s_key[excl] = ((u64)(hd[j] & ~kUnsortedBit) << lo_bits) | lo;
+        s_val[excl] = (unsigned)i;
+        ++excl;
+    }
+    __syncthreads();
+    const unsigned long long base = s_base;
+    for (unsigned t = threadIdx.x; t < total; t += kMKNT) {
+        keys[base + t] = s_key[t];
+        vals[base + t] = s_val[t];
+    }
 }
 
 // Dense ordinal of each list entry's group (runs of equal heads): exclusive
@@ -353,10 +405,10 @@ __global__ void __launch_bounds__(kUNT, sizeof(KeyT) == 4 ? 5 : 4) k_update(cons
         if (newf[j]) run = pos[j];
         unsigned v = vals[t];
         vv[j] = v;
-        hh[j] = (unsigned)run;
+        hh[j] = (unsigned)run | ((unsorted >> j & 1) ? kUnsortedBit : 0u);  // ISA value (flag: still tied)
         if (P) {
             sa[pos[j]] = v;
-            if (!be.stage) isa[v] = (unsigned)run;
+            if (!be.stage) isa[v] = hh[j];
         }
         if (unsorted >> j & 1) {
             // next round's inputs: slot, group head (= new isa) and suffix,
@@ -573,11 +625,11 @@ __global__ void k_lcp_patch(const u64 *__restrict__ stream, int b, const unsigne
     }
 }
 
-// isa[V[t]] = H[t]: members of groups still tied keep their group head.
+// isa[V[t]] = H[t] (flagged): members of groups still tied keep their group head.
 __global__ void k_isa_heads(const unsigned *__restrict__ V, const unsigned *__restrict__ H, long long U,
                             unsigned *__restrict__ isa) {
     const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t < U) isa[V[t]] = H[t];
+    if (t < U) isa[V[t]] = H[t] | kUnsortedBit;
 }
 
 // ---- small tied groups after round 0 ------------------------------------
@@ -1394,6 +1446,22 @@ void build_suffix_array(rs_ctx *c, long long n) {
         while ((1ull << g_bits) < ngroups) ++g_bits;
         int h_bits = 0;
         while ((1ull << h_bits) < (unsigned long long)n) ++h_bits;
+        // large rounds (most suffixes still tied): keys in text order, grouped
+        // by head slot; smaller rounds: the list gather (dense ordinals when
+        // they save radix passes)
+        const bool text_order = 4 * U > n && !std::getenv("RS_SA_LIST_KEYS");
+        if (text_order) {
+            unsigned long long *kc = (unsigned long long *)buf(c, B_SMALL, 4096) + 100;
+            RS_CUDA(cudaMemsetAsync(kc, 0, sizeof(*kc), c->stream));
+            RS_LAUNCH_B(c, 8.0 * n + 12.0 * U, k_make_keys_text, (unsigned)((n + kMKTile - 1) / kMKTile), kMKNT,
+                        0, isa, n, depth, lo_bits, k0, v0, kc);
+            unsigned long long got = 0;
+            fetch_small(c, &got, kc, sizeof(got));
+            if ((long long)got != U) fail(RS_ECUDA, "text-order round keys: tied-suffix count mismatch");
+            radix_sort_pairs<u64>(c, k0, k1, v0, v1, U, std::max(1, lo_bits + h_bits), &ks, &vs);
+            depth *= 2;
+            continue;
+        }
         const bool dense = (lo_bits + g_bits + 7) / 8 < (lo_bits + h_bits + 7) / 8;
         if (dense) {
             const long long gt = (U + kGTile - 1) / kGTile;
