@@ -332,24 +332,30 @@ def run_single(args) -> None:
     s_host = SuffixStructures(sa=sa, rank=rk, lcp=lc)
 
     def e2e_run(fn, reps):
-        out, res = [], None
+        """mean seconds per call over `reps` timed calls, the last result, and
+        the (h2d, d2h) bytes the library actually copied per timed call"""
+        out, res, xfer0 = [], None, None
         for i in range(args.warmup + reps):
             res = None
             ctx.synchronize()
+            if i == args.warmup:
+                xfer0 = ctx.transfer_bytes()
             t0 = time.perf_counter()
             res = fn()
             out.append(time.perf_counter() - t0)
-        return float(np.mean(out[args.warmup:])), res
+        xfer1 = ctx.transfer_bytes()
+        per = tuple((b - a) // reps for a, b in zip(xfer0, xfer1))
+        return float(np.mean(out[args.warmup:])), res, per
 
-    e2e_s, res = e2e_run(lambda: all_positions(t, mode="all", path="compact"), args.steps)
+    e2e_s, res, (e2e_h2d, e2e_d2h) = e2e_run(lambda: all_positions(t, mode="all", path="compact"), args.steps)
     parity = parity_of(args.config, n, res)
     assert int(res.flat_starts.size) == T
     del res
-    e2e_struct_s, res = e2e_run(
+    e2e_struct_s, res, (es_h2d, es_d2h) = e2e_run(
         lambda: all_positions(t, mode="all", path="compact", structures=s_host), max(3, args.steps // 3))
     assert int(res.flat_starts.size) == T
     del res
-    d2h = 8 * (n + 1) + 8 * (n + 2) + 8 * T
+    answer_bytes = 8 * (n + 1) + 8 * (n + 2) + 8 * T  # the int64 arrays the caller receives
 
     roof, rows = roofline_of(profile, args.steps)
     scan = next((r for r in rows if r["kernel"].startswith("k_query")), None)
@@ -369,13 +375,16 @@ def run_single(args) -> None:
                    "T": T},
         "gpu_launches": launches,
         "clocks": clk,
-        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n, "d2h_bytes_per_step": d2h,
-                "ms_per_step": 1e3 * e2e_s,
+        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
+                "ms_per_step": 1e3 * e2e_s, "answer_bytes_per_step": answer_bytes,
+                "bytes_counted": "rs_transfer_bytes: every host<->device copy the library issued in the timed calls "
+                                 "(answers cross PCIe as 1 byte per value when they fit, else 4; host threads "
+                                 "rebuild the int64 arrays)",
                 "path": "all_positions(Text, mode='all', path='compact') -- default call, host text in, "
                         "int64 numpy answers out (suffix sort + LCP + query on device, inside the timing)"},
         "e2e_structures_given": {
             "value": n / e2e_struct_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_struct_s,
-            "h2d_bytes_per_step": 16 * (n + 1) + 8, "d2h_bytes_per_step": d2h,
+            "h2d_bytes_per_step": es_h2d, "d2h_bytes_per_step": es_d2h,
             "path": "all_positions(Text, mode='all', path='compact', structures=SuffixStructures) -- "
                     "the reference arm's exact call"},
         "parity": parity,

@@ -67,6 +67,9 @@ const char *rs_last_error(const rs_ctx *ctx);
 int rs_synchronize(rs_ctx *ctx);
 /* number of kernels this context launched so far */
 int rs_launch_count(const rs_ctx *ctx, int64_t *count);
+/* bytes this context copied host -> device and device -> host so far (every
+ * transfer the library issues: inputs, wire words / bytes, small readbacks) */
+int rs_transfer_bytes(const rs_ctx *ctx, int64_t *h2d_bytes, int64_t *d2h_bytes);
 /* last per-stage device times (RS_NUM_STAGES doubles) */
 int rs_stage_times(const rs_ctx *ctx, double *ms);
 /* CUDA-event timing on the context stream (slots 0..63) */

@@ -37,6 +37,7 @@ SIGNATURES = {
     "rs_last_error": [_CTX],
     "rs_synchronize": [_CTX],
     "rs_launch_count": [_CTX, _I64P],
+    "rs_transfer_bytes": [_CTX, _I64P, _I64P],
     "rs_stage_times": [_CTX, ctypes.POINTER(ctypes.c_double)],
     "rs_record_event": [_CTX, ctypes.c_int],
     "rs_elapsed_ms": [_CTX, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float)],
@@ -176,6 +177,12 @@ class Context:
         v = ctypes.c_int64()
         self.call("rs_launch_count", ctypes.byref(v))
         return int(v.value)
+
+    def transfer_bytes(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes copied by this context so far."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self.call("rs_transfer_bytes", ctypes.byref(a), ctypes.byref(b))
+        return int(a.value), int(b.value)
 
     def stage_times(self) -> dict:
         arr = (ctypes.c_double * len(STAGES))()

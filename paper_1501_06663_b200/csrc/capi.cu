@@ -48,6 +48,8 @@ bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long c
                     long long add);
 void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes);
 void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add);
+bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
+                     long long L, long long T, long long *lengths, long long *offsets, long long *flat);
 
 void nccl_unique_id(unsigned char *out);
 void nccl_init(rs_ctx *c, const unsigned char *id_bytes, int rank, int world);
@@ -91,6 +93,7 @@ void *buf(rs_ctx *c, BufId id, size_t bytes) {
 void fetch_small(rs_ctx *c, void *host, const void *dev, size_t bytes) {
     if (bytes > 65536) fail(RS_EINVAL, "fetch_small too large");
     RS_CUDA(cudaMemcpyAsync(c->small_host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += (long long)bytes;
     RS_CUDA(cudaStreamSynchronize(c->stream));
     memcpy(host, c->small_host, bytes);
 }
@@ -205,9 +208,11 @@ void check_n(long long n) {
 
 void h2d(rs_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += (long long)bytes;
 }
 void d2h(rs_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += (long long)bytes;
 }
 
 void invalidate(rs_ctx *c) {
@@ -347,6 +352,13 @@ int rs_synchronize(rs_ctx *c) {
 int rs_launch_count(const rs_ctx *c, int64_t *count) {
     if (!c || !count) return RS_EINVAL;
     *count = c->launches;
+    return RS_OK;
+}
+
+int rs_transfer_bytes(const rs_ctx *c, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    if (!c || !h2d_bytes || !d2h_bytes) return RS_EINVAL;
+    *h2d_bytes = c->h2d_bytes;
+    *d2h_bytes = c->d2h_bytes;
     return RS_OK;
 }
 
@@ -744,6 +756,10 @@ int rs_fetch_all(rs_ctx *c, int64_t *lengths, int64_t *offsets, int64_t *flat) {
     return guarded(c, [&] {
         if (c->out_mode != 1) fail(RS_ESTATE, "no all-ties results on device");
         long long n = c->n;
+        if (fetch_csr_bytes(c, (const long long *)c->bufs[B_OUT0].p, (const long long *)c->bufs[B_OUT1].p,
+                            (const long long *)c->bufs[B_FLAT].p, n + 1, c->total, (long long *)lengths,
+                            (long long *)offsets, (long long *)flat))
+            return;
         fetch_i64(c, (long long *)lengths, (const long long *)c->bufs[B_OUT0].p, n + 1, 0);
         fetch_i64(c, (long long *)offsets, (const long long *)c->bufs[B_OUT1].p, n + 2, 2);
         fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);
@@ -1050,6 +1066,9 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
         long long cnt = c->shard_hi - c->shard_lo;
         const long long *o0 = (const long long *)c->bufs[B_OUT0].p, *o1 = (const long long *)c->bufs[B_OUT1].p;
         if (mode == RS_MODE_ALL) {
+            if (fetch_csr_bytes(c, o0, o1, (const long long *)c->bufs[B_FLAT].p, cnt, c->total, (long long *)a,
+                                (long long *)b, (long long *)flat))
+                return;
             fetch_i64(c, (long long *)a, o0, cnt, 0);
             fetch_i64(c, (long long *)b, o1, cnt + 1, 2);
             fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);

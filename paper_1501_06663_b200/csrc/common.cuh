@@ -71,6 +71,7 @@ enum BufId {
     B_SEND,      // distributed sort: (position, raw) entries bound for other ranks
     B_XFER,      // host_io.cu: two-slot device ring of 32-bit wire words
     B_XFER_ENDS, // host_io.cu: first / last value of every chunk
+    B_WIRE,      // host_io.cu: byte-wide wire copy of the all-ties CSR
     B_COUNT
 };
 
@@ -98,6 +99,7 @@ struct rs_ctx {
     cudaEvent_t xfer_ev[2] = {nullptr, nullptr};
     cudaStream_t xfer_side = nullptr;                // host_io.cu direct-DMA side stream
     cudaEvent_t xfer_side_ev = nullptr;
+    long long h2d_bytes = 0, d2h_bytes = 0;         // host <-> device bytes copied (rs_transfer_bytes)
     // pipeline state
     long long n = -1;
     bool have_text = false;
@@ -123,14 +125,14 @@ struct rs_ctx {
     bool isa_lazy = false;                  // B_ISA not built (device SA without later rounds): fill from SA on demand
     long long sa_unsorted_after_round0 = 0; // suffixes left in tied groups by round 0
     long long sa_final_depth = 0;          // sorted depth when prefix doubling stopped
-    bool lcp_from_keys = false;
-    bool sa_device_built = false;
-    bool sa_isa_consistent = false;
-    long long max_lcp = -1;                  // max of the resident LCP (-1: not computed)          // caller sa/rank checked to be inverse permutations
-    bool raw_from_round0 = false;
+    bool lcp_from_keys = false;             // B_LCP holds round-0 key LCPs (+ unknown marks)
+    bool sa_device_built = false;           // SA/ISA/LCP built here (mutually consistent)
+    bool sa_isa_consistent = false;         // caller sa/rank checked to be inverse permutations
+    long long max_lcp = -1;                 // max of the resident LCP (-1: not computed)
+    bool raw_from_round0 = false;           // B_RAW filled during the SA build (+ LCP patch fix-up)
     long long tsv_bytes = 0;
     long long patch_slots = 0;              // tied slots of round 0 kept in B_PATCH
-    bool out_ref_layout = false;            // B_OUT* hold the reference 1-based layout           // B_RAW filled during the SA build (+ LCP patch fix-up)           // SA/ISA/LCP built here (mutually consistent)             // B_LCP holds round-0 key LCPs (+ unknown marks)
+    bool out_ref_layout = false;            // B_OUT* hold the reference 1-based layout
     // per-kernel profiling (CUDA events around every launch while enabled)
     bool profiling = false;
     struct ProfRec {
@@ -269,20 +271,22 @@ __device__ u64 lookback_warp(u64 *status, long long tile, u64 aggregate, Op op, 
     long long base = tile - 1;
     while (true) {
         long long idx = base - lane;
-        u64 s;
-        if (idx >= 0) {
-            s = ld_relaxed(&status[idx]);
-            unsigned ns = 32;  // exponential backoff: a waiting warp issues few instructions
-            while ((s >> 62) == 0) {
-                __nanosleep(ns);
-                ns = ns < 512 ? 2 * ns : ns;
-                s = ld_relaxed(&status[idx]);
-            }
-        } else {
-            s = kFlagPre | Op::identity;
+        u64 s = idx >= 0 ? ld_relaxed(&status[idx]) : (kFlagPre | Op::identity);
+        unsigned pre, ns = 32;
+        int first;
+        // wait only for the predecessors up to the nearest inclusive prefix:
+        // tiles before it do not matter (waiting for all 32 lanes made a tile
+        // spin ~170 times on neighbours it never needed)
+        while (true) {
+            pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+            first = pre ? __ffs(pre) - 1 : 32;
+            const unsigned need = first == 32 ? 0xffffffffu : (2u << first) - 1u;
+            const unsigned waiting = __ballot_sync(0xffffffffu, (s >> 62) == 0) & need;
+            if (!waiting) break;
+            __nanosleep(ns);  // exponential backoff: a waiting warp issues few instructions
+            ns = ns < 512 ? 2 * ns : ns;
+            if (waiting >> lane & 1) s = ld_relaxed(&status[idx]);
         }
-        unsigned pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-        int first = pre ? __ffs(pre) - 1 : 32;
         u64 v = (lane <= first) ? (s & kValMask) : Op::identity;
         v = warp_reduce(v, op);
         exclusive = op(exclusive, v);
@@ -325,18 +329,19 @@ __device__ __noinline__ static u64 lookback_warp_wide(u64 *st, long long tiles, 
     long long base = tile - 1;
     while (true) {
         long long idx = base - lane;
-        u64 f = 2, v = 0;
-        if (idx >= 0) {
-            f = ld_acquire(&flag[idx]);
-            while (f == 0) {
-                __nanosleep(20);
-                f = ld_acquire(&flag[idx]);
-            }
-            v = ld_relaxed(f == 2 ? &incl[idx] : &agg[idx]);
+        u64 f = idx >= 0 ? ld_acquire(&flag[idx]) : 2, v = 0;
+        unsigned pre;
+        int first;
+        while (true) {  // wait only for the lanes up to the nearest inclusive prefix
+            pre = __ballot_sync(0xffffffffu, f == 2);
+            first = pre ? __ffs(pre) - 1 : 32;
+            const unsigned need = first == 32 ? 0xffffffffu : (2u << first) - 1u;
+            const unsigned waiting = __ballot_sync(0xffffffffu, f == 0) & need;
+            if (!waiting) break;
+            __nanosleep(20);
+            if (waiting >> lane & 1) f = ld_acquire(&flag[idx]);
         }
-        unsigned pre = __ballot_sync(0xffffffffu, f == 2);
-        int first = pre ? __ffs(pre) - 1 : 32;
-        v = (lane <= first) ? v : 0;
+        if (idx >= 0 && lane <= first) v = ld_relaxed(f == 2 ? &incl[idx] : &agg[idx]);
         v = warp_reduce(v, OpSum());
         exclusive += v;
         if (pre) break;

@@ -35,14 +35,18 @@ namespace rsb {
 // host_widen.cpp: out[j] = f(w[j]) + add, streaming stores
 void widen_words(const unsigned *w, long long *out, long long x, long long y, int mode, unsigned w0,
                  long long add);
+void widen_bytes(const unsigned char *w, long long *out, long long x, long long y);
+void prefix_bytes(const unsigned char *w, long long *out, long long x, long long y, long long start, bool is_signed);
 
 namespace {
 
 void h2d(rs_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += (long long)bytes;
 }
 void d2h(rs_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes) RS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += (long long)bytes;
 }
 
 // ---- host thread pool: run(f) calls f(t, T) on T threads and waits ----------
@@ -183,6 +187,7 @@ void pipeline_out(rs_ctx *c, long long count, Issue issue, Widen widen, long lon
         const long long a = i * kChunk, len = std::min(kChunk, count - a);
         const void *d = issue(a, len, (int)(i & 1));
         RS_CUDA(cudaMemcpyAsync(s.host[i & 1], d, 4 * (size_t)len, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += 4 * len;
         RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
     };
     start(0);
@@ -237,6 +242,7 @@ void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count
         RS_CUDA(cudaEventRecord(c->xfer_side_ev, c->stream));  // after the producing kernels
         RS_CUDA(cudaStreamWaitEvent(c->xfer_side, c->xfer_side_ev, 0));
         RS_CUDA(cudaMemcpyAsync(dst, dsrc, 8 * (size_t)direct, cudaMemcpyDeviceToHost, c->xfer_side));
+        c->d2h_bytes += 8 * direct;
     }
     if (count > direct) fetch_i64_staged(c, dst + direct, dsrc + direct, count - direct, kind);
     if (direct > 0) RS_CUDA(cudaStreamSynchronize(c->xfer_side));
@@ -291,6 +297,119 @@ void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long
         dst);
 }
 
+// ---- byte wire for the all-ties CSR --------------------------------------
+//
+// With short repeats (every length, tie count and start-to-start step below
+// 2^7 .. 2^8 -- i.i.d. DNA has max LLR ~ 28) the three CSR arrays travel as ONE
+// byte per value: lengths as u8, offsets as u8 tie counts (offsets[k+1] -
+// offsets[k]), tie starts as i8 differences of consecutive starts.  The host
+// rebuilds offsets and starts with running sums, restarting every kSample
+// values from an exact int64 sample taken on the device.  4.2 GB of 32-bit
+// wire words become 1.05 GB on C3, and the host's memory traffic (DMA in,
+// read, int64 out) drops from ~16.8 GB to ~10.5 GB.  If any value does not fit
+// the caller falls back to the 32-bit wire.
+constexpr long long kSample = 1ll << 16;
+
+__global__ void k_wire_len_cnt(const long long *__restrict__ len, const long long *__restrict__ off, long long count,
+                               unsigned char *__restrict__ len8, unsigned char *__restrict__ cnt8,
+                               long long *__restrict__ osamp, unsigned *__restrict__ bad) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    bool b = false;
+    if (k < count) {
+        const long long L = len[k], o = off[k], C = off[k + 1] - o;
+        b = (unsigned long long)L > 255ull || (unsigned long long)C > 255ull;
+        len8[k] = (unsigned char)L;
+        cnt8[k] = (unsigned char)C;
+        if ((k & (kSample - 1)) == 0) osamp[k / kSample] = o;
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+__global__ void k_wire_flat(const long long *__restrict__ flat, long long T, unsigned char *__restrict__ d8,
+                            long long *__restrict__ fsamp, unsigned *__restrict__ bad) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    bool b = false;
+    if (t < T) {
+        const long long v = flat[t];
+        long long d = 0;
+        if (t > 0) {
+            d = v - flat[t - 1];
+            b = d < -128 || d > 127;
+        }
+        d8[t] = (unsigned char)(signed char)d;
+        if ((t & (kSample - 1)) == 0) fsamp[t / kSample] = v;
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+// D2H of `count` wire bytes through the two pinned slots; decode(w, a, x, y)
+// rebuilds values [a + x, a + y) from the slot holding bytes [a, a + len),
+// x a multiple of kSample, on the host threads while the next DMA runs.
+template <typename Decode>
+static void pipeline_bytes(rs_ctx *c, const unsigned char *dsrc, long long count, Decode decode) {
+    const long long ch = 4 * kChunk;  // bytes per slot (a multiple of kSample)
+    const long long nch = (count + ch - 1) / ch;
+    Stage s = stage(c);
+    auto start = [&](long long i) {
+        const long long a = i * ch, len = std::min(ch, count - a);
+        RS_CUDA(cudaMemcpyAsync(s.host[i & 1], dsrc + a, (size_t)len, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += len;
+        RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
+    };
+    start(0);
+    if (nch > 1) start(1);
+    Pool &pool = Pool::get();
+    for (long long i = 0; i < nch; ++i) {
+        RS_CUDA(cudaEventSynchronize(s.ev[i & 1]));
+        const long long a = i * ch, len = std::min(ch, count - a);
+        const unsigned char *w = (const unsigned char *)s.host[i & 1];
+        const long long blocks = (len + kSample - 1) / kSample;
+        pool.run([&](int t, int T) {
+            long long bx, by;
+            split(blocks, t, T, bx, by);
+            const long long x = bx * kSample, y = std::min(len, by * kSample);
+            if (y > x) decode(w, a, x, y);
+        });
+        if (i + 2 < nch) start(i + 2);
+    }
+}
+
+// CSR answers (lengths[L], offsets[L + 1], flat[T]) from device int64 arrays
+// over the byte wire; false (nothing written) when a value does not fit.
+bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
+                     long long L, long long T, long long *lengths, long long *offsets, long long *flat) {
+    if (L < (4ll << 20) || std::getenv("RS_WORD_WIRE")) return false;
+    const long long ns = (L + kSample - 1) / kSample, ts = (T + kSample - 1) / kSample;
+    unsigned char *w = (unsigned char *)buf(c, B_WIRE, (size_t)(2 * L + T) + 16 * (size_t)(ns + ts + 2) + 64);
+    unsigned char *len8 = w, *cnt8 = w + L, *d8 = w + 2 * L;
+    long long *osamp = (long long *)(((uintptr_t)(d8 + T) + 15) & ~(uintptr_t)15);
+    long long *fsamp = osamp + ns;
+    unsigned *bad = (unsigned *)(fsamp + ts + 1);
+    RS_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), c->stream));
+    RS_LAUNCH_B(c, 25.0 * (double)L, k_wire_len_cnt, grid_for(L, 256), 256, 0, d_len, d_off, L, len8, cnt8, osamp,
+                bad);
+    if (T > 0) RS_LAUNCH_B(c, 9.0 * (double)T, k_wire_flat, grid_for(T, 256), 256, 0, d_flat, T, d8, fsamp, bad);
+    std::vector<long long> samp((size_t)(ns + ts));
+    unsigned hbad = 0;
+    d2h(c, &hbad, bad, sizeof(hbad));
+    d2h(c, samp.data(), osamp, sizeof(long long) * (size_t)(ns + ts));
+    RS_CUDA(cudaStreamSynchronize(c->stream));
+    if (hbad) return false;
+    const long long *os = samp.data(), *fs = samp.data() + ns;
+    pipeline_bytes(c, len8, L, [&](const unsigned char *b, long long a, long long x, long long y) {
+        widen_bytes(b, lengths + a, x, y);
+    });
+    offsets[0] = os[0];
+    pipeline_bytes(c, cnt8, L, [&](const unsigned char *b, long long a, long long x, long long y) {
+        prefix_bytes(b, offsets + 1 + a, x, y, os[(a + x) / kSample], false);
+    });
+    if (T > 0)
+        pipeline_bytes(c, d8, T, [&](const unsigned char *b, long long a, long long x, long long y) {
+            prefix_bytes(b, flat + a, x, y, fs[(a + x) / kSample] - (long long)(signed char)b[x], true);
+        });
+    return true;
+}
+
 // H2D of `count` int64 values into a device u32 array, each checked to lie in
 // [lo, hi] and stored as value + add.  Returns false (nothing usable written)
 // if a value is out of range.
@@ -322,6 +441,7 @@ bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long c
             return false;
         }
         RS_CUDA(cudaMemcpyAsync(ddst + a, w, 4 * (size_t)len, cudaMemcpyHostToDevice, c->stream));
+        c->h2d_bytes += 4 * len;
         RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
     }
     RS_CUDA(cudaStreamSynchronize(c->stream));
@@ -356,6 +476,7 @@ void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes) {
             if (y > x) std::memcpy(w + x, in + x, (size_t)(y - x));
         });
         RS_CUDA(cudaMemcpyAsync((char *)ddst + a, w, len, cudaMemcpyHostToDevice, c->stream));
+        c->h2d_bytes += (long long)len;
         RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
     }
 }

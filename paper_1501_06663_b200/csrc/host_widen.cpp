@@ -79,4 +79,82 @@ void widen_words(const unsigned *w, long long *out, long long x, long long y, in
     else widen_scalar<0>(w, out, x, y, w0, add);
 }
 
+// ---- byte wire decoders (host_io.cu fetch_all_bytes) ----------------------
+
+// out[j] = w[j] for j in [x, y)
+__attribute__((target("avx2"))) static void widen_u8_avx2(const unsigned char *w, long long *out, long long x,
+                                                           long long y) {
+    long long j = x;
+    while (j < y && (reinterpret_cast<uintptr_t>(out + j) & 31)) {
+        out[j] = w[j];
+        ++j;
+    }
+    for (; j + 16 <= y; j += 16) {
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i *>(w + j));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(out + j), _mm256_cvtepu8_epi64(b));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(out + j + 4), _mm256_cvtepu8_epi64(_mm_srli_si128(b, 4)));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(out + j + 8), _mm256_cvtepu8_epi64(_mm_srli_si128(b, 8)));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(out + j + 12), _mm256_cvtepu8_epi64(_mm_srli_si128(b, 12)));
+    }
+    for (; j < y; ++j) out[j] = w[j];
+    _mm_sfence();
+}
+
+void widen_bytes(const unsigned char *w, long long *out, long long x, long long y) {
+    if (y <= x) return;
+    if (have_avx2()) {
+        widen_u8_avx2(w, out, x, y);
+        return;
+    }
+    for (long long j = x; j < y; ++j) out[j] = w[j];
+}
+
+// Running sums: out[j] = start + w[x] + ... + w[j] (SIGNED: w as int8).
+// 8 values per step: an in-register prefix over 32-bit lanes (relative to the
+// step's carry-in; a step adds at most 8 * 255), widened to int64 and stored
+// with streaming stores.
+template <bool SIGNED>
+__attribute__((target("avx2"))) static void prefix_avx2(const unsigned char *w, long long *out, long long x,
+                                                        long long y, long long run) {
+    long long j = x;
+    while (j < y && (reinterpret_cast<uintptr_t>(out + j) & 31)) {
+        run += SIGNED ? (long long)(signed char)w[j] : (long long)w[j];
+        out[j] = run;
+        ++j;
+    }
+    for (; j + 8 <= y; j += 8) {
+        const __m128i b = _mm_loadl_epi64(reinterpret_cast<const __m128i *>(w + j));
+        __m256i v = SIGNED ? _mm256_cvtepi8_epi32(b) : _mm256_cvtepu8_epi32(b);
+        v = _mm256_add_epi32(v, _mm256_slli_si256(v, 4));  // prefix within each 128-bit half
+        v = _mm256_add_epi32(v, _mm256_slli_si256(v, 8));
+        const __m256i lowtot = _mm256_permutevar8x32_epi32(v, _mm256_set1_epi32(3));
+        v = _mm256_add_epi32(v, _mm256_blend_epi32(_mm256_setzero_si256(), lowtot, 0xF0));
+        const __m256i base = _mm256_set1_epi64x(run);
+        const __m256i lo = _mm256_add_epi64(base, _mm256_cvtepi32_epi64(_mm256_castsi256_si128(v)));
+        const __m256i hi = _mm256_add_epi64(base, _mm256_cvtepi32_epi64(_mm256_extracti128_si256(v, 1)));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(out + j), lo);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(out + j + 4), hi);
+        run += (long long)_mm256_extract_epi32(v, 7);
+    }
+    for (; j < y; ++j) {
+        run += SIGNED ? (long long)(signed char)w[j] : (long long)w[j];
+        out[j] = run;
+    }
+    _mm_sfence();
+}
+
+void prefix_bytes(const unsigned char *w, long long *out, long long x, long long y, long long start, bool is_signed) {
+    if (y <= x) return;
+    if (have_avx2()) {
+        if (is_signed) prefix_avx2<true>(w, out, x, y, start);
+        else prefix_avx2<false>(w, out, x, y, start);
+        return;
+    }
+    long long run = start;
+    for (long long j = x; j < y; ++j) {
+        run += is_signed ? (long long)(signed char)w[j] : (long long)w[j];
+        out[j] = run;
+    }
+}
+
 }  // namespace rsb

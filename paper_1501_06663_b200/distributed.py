@@ -572,10 +572,13 @@ def bench_main(args) -> None:
     # ---- e2e: the API-level call with host buffers ----
     e2e = []
     res = None
+    xfer0 = None
     for i in range(args.warmup + max(1, args.steps)):
         res = None
         dist.barrier()
         torch.cuda.synchronize()
+        if i == args.warmup:
+            xfer0 = ctx.transfer_bytes()
         t0 = time.perf_counter()
         res = replicated_all_positions(data if rank == 0 else None, "all")
         torch.cuda.synchronize()
@@ -584,6 +587,10 @@ def bench_main(args) -> None:
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         if i >= args.warmup:
             e2e.append(float(dt.item()))
+    # bytes the library copied host<->device in the timed calls, summed over ranks
+    xfer = torch.tensor([b - a for a, b in zip(xfer0, ctx.transfer_bytes())], dtype=torch.float64, device=device)
+    dist.all_reduce(xfer, op=dist.ReduceOp.SUM)
+    h2d_step, d2h_step = (int(v) // max(1, args.steps) for v in xfer.tolist())
     if rank == 0:
         assert int(res.flat_starts.size) == T, (res.flat_starts.size, T)
         line = {
@@ -600,8 +607,8 @@ def bench_main(args) -> None:
                        "T": T},
             "gpu_launches": int(round(float(lt.item()))),
             "stages_ms_rank0": stages,
-            "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": n,
-                    "d2h_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
+            "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": h2d_step,
+                    "d2h_bytes_per_step": d2h_step, "answer_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
                     "ms_per_step": 1e3 * float(np.mean(e2e)),
                     "path": "replicated_all_positions: text H2D on rank 0 + NCCL broadcast, suffix "
                             "structures + shard query on every GPU, per-rank D2H into one shared host "

@@ -8,6 +8,7 @@ checked against the pinned C oracle or reference digests.
 from __future__ import annotations
 
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -710,3 +711,83 @@ def test_new_entry_points_errors():
             ctx.call("rs_set_structures", _native.i64(s.sa), _native.i64(rank), _native.i64(s.lcp), data.size)
     finally:
         ctx.close()
+
+
+def _all_with_wire(t, word: bool):
+    from paper_1501_06663_b200 import _native
+    ctx = _native.context()
+    prev = os.environ.pop("RS_WORD_WIRE", None)
+    if word:
+        os.environ["RS_WORD_WIRE"] = "1"
+    try:
+        x0 = ctx.transfer_bytes()
+        A = rb.all_positions(t, mode="all", path="compact")
+        x1 = ctx.transfer_bytes()
+    finally:
+        os.environ.pop("RS_WORD_WIRE", None)
+        if prev is not None:
+            os.environ["RS_WORD_WIRE"] = prev
+    return A, x1[1] - x0[1]
+
+
+@pytest.mark.parametrize("kind", ["iid", "planted", "fibonacci"])
+def test_byte_wire_matches_word_wire(kind):
+    """csrc/host_io.cu fetch_csr_bytes: the all-ties CSR crosses PCIe as one
+    byte per value (u8 lengths, u8 tie counts, i8 start steps; int64 samples
+    every 2^16 values) and the host rebuilds the int64 arrays.  Identical to
+    the 32-bit wire; a text whose values do not fit (long repeats: Fibonacci)
+    falls back to the 32-bit wire by itself."""
+    data = {"iid": lambda: workloads.iid_dna(9_000_000, 41),
+            "planted": lambda: workloads.planted_dna(6_000_000, 4, family_len=300),
+            "fibonacci": lambda: workloads.fibonacci_mutated(5_000_000, 3, rate=1e-4)}[kind]()
+    t = rb.Text(data)
+    A, d2h_bytes = _all_with_wire(t, word=False)
+    W, d2h_words = _all_with_wire(t, word=True)
+    assert np.array_equal(A.lengths, W.lengths) and np.array_equal(A.offsets, W.offsets)
+    assert np.array_equal(A.flat_starts, W.flat_starts)
+    n, T = data.size, A.flat_starts.size
+    assert d2h_words >= 4 * (2 * n + T)  # 32-bit words (+ small readbacks)
+    if kind == "iid":  # short repeats: the byte wire was used
+        assert d2h_bytes < 2 * n + T + (1 << 20), (d2h_bytes, n, T)
+    if kind == "fibonacci":  # lengths far above 255: 32-bit wire
+        assert int(A.lengths.max()) > 255 and d2h_bytes >= 4 * (2 * n + T)
+    from paper_1501_06663_b200.query import count_wrong_answers
+    c = rb.build_compact_llr(rb.build_raw_llr(rb.build_suffix_structures(t)))
+    assert count_wrong_answers(c, n, all_answers=A) == 0
+
+
+def test_byte_wire_shards():
+    """rs_fetch_shard over the byte wire (shards of >= 4 Mi positions, CSR
+    offsets rebased on device): stitched shards == the full answer."""
+    from paper_1501_06663_b200 import _native
+    from paper_1501_06663_b200 import distributed as D
+    data = workloads.iid_dna(9_000_000, 43)
+    n = data.size
+    full = rb.all_positions(rb.Text(data), mode="all", path="compact")
+    ctx = _native.context()
+    with ctx.lock:
+        ctx.call("rs_set_text", _native.u8(data), n)
+        ctx.call("rs_build_structures")
+    lengths = np.zeros(n + 1, np.int64)
+    offsets = np.zeros(n + 2, np.int64)
+    flats, base = [], 0
+    for r in range(2):
+        lo, hi = D.shard_range(n, 2, r)
+        with ctx.lock:
+            tot = np.zeros(1, np.int64)
+            ctx.call("rs_query_structures_shard", 1, lo, hi, _native.i64(tot))
+            ctx.call("rs_shard_rebase", base)
+            a = np.zeros(hi - lo, np.int64)
+            b = np.zeros(hi - lo + 1, np.int64)
+            f = np.zeros(int(tot[0]), np.int64)
+            x0 = ctx.transfer_bytes()
+            ctx.call("rs_fetch_shard", 1, _native.i64(a), _native.i64(b), _native.i64(f))
+            x1 = ctx.transfer_bytes()
+        assert x1[1] - x0[1] < 2 * (hi - lo) + f.size + (1 << 20)  # byte wire
+        assert b[0] == base
+        lengths[lo:hi] = a
+        offsets[lo + 1:hi + 1] = b[1:]
+        flats.append(f)
+        base += f.size
+    assert np.array_equal(lengths, full.lengths) and np.array_equal(offsets, full.offsets)
+    assert np.array_equal(np.concatenate(flats), full.flat_starts)
