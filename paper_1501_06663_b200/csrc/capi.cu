@@ -50,6 +50,8 @@ void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes);
 void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add);
 bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
                      long long L, long long T, long long *lengths, long long *offsets, long long *flat);
+bool fetch_leftmost_bytes(rs_ctx *c, const long long *d_starts, const long long *d_len, long long L, long long pos0,
+                          long long *starts, long long *lengths);
 
 void nccl_unique_id(unsigned char *out);
 void nccl_init(rs_ctx *c, const unsigned char *id_bytes, int rank, int world);
@@ -747,6 +749,9 @@ int rs_fetch_leftmost(rs_ctx *c, int64_t *starts, int64_t *lengths) {
     return guarded(c, [&] {
         if (c->out_mode != 0) fail(RS_ESTATE, "no leftmost results on device");
         long long n = c->n;
+        if (fetch_leftmost_bytes(c, (const long long *)c->bufs[B_OUT0].p, (const long long *)c->bufs[B_OUT1].p,
+                                 n + 1, 0, (long long *)starts, (long long *)lengths))
+            return;
         fetch_i64(c, (long long *)starts, (const long long *)c->bufs[B_OUT0].p, n + 1, 1);
         fetch_i64(c, (long long *)lengths, (const long long *)c->bufs[B_OUT1].p, n + 1, 0);
     });
@@ -1073,6 +1078,7 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
             fetch_i64(c, (long long *)b, o1, cnt + 1, 2);
             fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);
         } else {
+            if (fetch_leftmost_bytes(c, o0, o1, cnt, c->shard_lo, (long long *)a, (long long *)b)) return;
             fetch_i64(c, (long long *)a, o0, cnt, 1);
             fetch_i64(c, (long long *)b, o1, cnt, 0);
         }

@@ -37,6 +37,8 @@ void widen_words(const unsigned *w, long long *out, long long x, long long y, in
                  long long add);
 void widen_bytes(const unsigned char *w, long long *out, long long x, long long y);
 void prefix_bytes(const unsigned char *w, long long *out, long long x, long long y, long long start, bool is_signed);
+void leftmost_pairs(const unsigned char *w, long long *starts, long long *lengths, long long x, long long y,
+                    long long pos_x);
 
 namespace {
 
@@ -342,6 +344,22 @@ __global__ void k_wire_flat(const long long *__restrict__ flat, long long T, uns
     if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
 
+// leftmost answers as byte pairs: w[2j] = length, w[2j+1] = position - start
+// (slot j answers position pos0 + j; a zero length means start -1)
+__global__ void k_wire_leftmost(const long long *__restrict__ starts, const long long *__restrict__ lengths,
+                                long long count, long long pos0, unsigned char *__restrict__ w,
+                                unsigned *__restrict__ bad) {
+    const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    bool b = false;
+    if (j < count) {
+        const long long L = lengths[j], d = L ? pos0 + j - starts[j] : 0;
+        b = (unsigned long long)L > 255ull || (unsigned long long)d > 255ull;
+        w[2 * j] = (unsigned char)L;
+        w[2 * j + 1] = (unsigned char)d;
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
 // D2H of `count` wire bytes through the two pinned slots; decode(w, a, x, y)
 // rebuilds values [a + x, a + y) from the slot holding bytes [a, a + len),
 // x a multiple of kSample, on the host threads while the next DMA runs.
@@ -407,6 +425,28 @@ bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, 
         pipeline_bytes(c, d8, T, [&](const unsigned char *b, long long a, long long x, long long y) {
             prefix_bytes(b, flat + a, x, y, fs[(a + x) / kSample] - (long long)(signed char)b[x], true);
         });
+    return true;
+}
+
+// Leftmost answers (starts[L], lengths[L], slot j = position pos0 + j) over
+// the byte wire (2 bytes per position instead of 8 + 8 in memory, 4 + 4 on the
+// 32-bit wire); false (nothing written) when a value does not fit.
+bool fetch_leftmost_bytes(rs_ctx *c, const long long *d_starts, const long long *d_len, long long L, long long pos0,
+                          long long *starts, long long *lengths) {
+    if (L < (4ll << 20) || std::getenv("RS_WORD_WIRE")) return false;
+    unsigned char *w = (unsigned char *)buf(c, B_WIRE, (size_t)(2 * L) + 64);
+    unsigned *bad = (unsigned *)(((uintptr_t)(w + 2 * L) + 15) & ~(uintptr_t)15);
+    RS_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), c->stream));
+    RS_LAUNCH_B(c, 18.0 * (double)L, k_wire_leftmost, grid_for(L, 256), 256, 0, d_starts, d_len, L, pos0, w, bad);
+    unsigned hbad = 0;
+    d2h(c, &hbad, bad, sizeof(hbad));
+    RS_CUDA(cudaStreamSynchronize(c->stream));
+    if (hbad) return false;
+    pipeline_bytes(c, w, 2 * L, [&](const unsigned char *b, long long a, long long x, long long y) {
+        // byte offsets [a + x, a + y) are slots [(a + x) / 2, (a + y) / 2)
+        const long long j0 = (a + x) / 2;
+        leftmost_pairs(b + x, starts + j0, lengths + j0, 0, (y - x) / 2, pos0 + j0);
+    });
     return true;
 }
 

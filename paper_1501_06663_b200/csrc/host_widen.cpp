@@ -157,4 +157,46 @@ void prefix_bytes(const unsigned char *w, long long *out, long long x, long long
     }
 }
 
+// Leftmost answers from (length, distance) byte pairs: lengths[j] = w[2j],
+// starts[j] = pos_x + j - w[2j+1] (or -1 when the length is 0), j in [x, y).
+__attribute__((target("avx2"))) static void leftmost_avx2(const unsigned char *w, long long *starts,
+                                                          long long *lengths, long long x, long long y,
+                                                          long long pos_x) {
+    long long j = x;
+    auto one = [&](long long i) {
+        const unsigned L = w[2 * i], d = w[2 * i + 1];
+        lengths[i] = L;
+        starts[i] = L ? pos_x + (i - x) - (long long)d : -1ll;
+    };
+    while (j < y && ((reinterpret_cast<uintptr_t>(starts + j) | reinterpret_cast<uintptr_t>(lengths + j)) & 31)) one(j++);
+    const __m256i step = _mm256_set_epi64x(3, 2, 1, 0), minus1 = _mm256_set1_epi64x(-1);
+    const __m128i lo_mask = _mm_set1_epi16(0x00ff);
+    for (; j + 4 <= y; j += 4) {
+        const __m128i p = _mm_loadl_epi64(reinterpret_cast<const __m128i *>(w + 2 * j));  // 4 pairs
+        const __m128i len16 = _mm_and_si128(p, lo_mask), d16 = _mm_srli_epi16(p, 8);
+        const __m256i L = _mm256_cvtepu16_epi64(len16), D = _mm256_cvtepu16_epi64(d16);
+        const __m256i pos = _mm256_add_epi64(_mm256_set1_epi64x(pos_x + (j - x)), step);
+        const __m256i st = _mm256_sub_epi64(pos, D);
+        const __m256i none = _mm256_cmpeq_epi64(L, _mm256_setzero_si256());
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(lengths + j), L);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(starts + j), _mm256_blendv_epi8(st, minus1, none));
+    }
+    for (; j < y; ++j) one(j);
+    _mm_sfence();
+}
+
+void leftmost_pairs(const unsigned char *w, long long *starts, long long *lengths, long long x, long long y,
+                    long long pos_x) {
+    if (y <= x) return;
+    if (have_avx2()) {
+        leftmost_avx2(w, starts, lengths, x, y, pos_x);
+        return;
+    }
+    for (long long j = x; j < y; ++j) {
+        const unsigned L = w[2 * j], d = w[2 * j + 1];
+        lengths[j] = L;
+        starts[j] = L ? pos_x + (j - x) - (long long)d : -1ll;
+    }
+}
+
 }  // namespace rsb

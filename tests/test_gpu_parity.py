@@ -713,7 +713,7 @@ def test_new_entry_points_errors():
         ctx.close()
 
 
-def _all_with_wire(t, word: bool):
+def _all_with_wire(t, word: bool, mode: str = "all"):
     from paper_1501_06663_b200 import _native
     ctx = _native.context()
     prev = os.environ.pop("RS_WORD_WIRE", None)
@@ -721,7 +721,7 @@ def _all_with_wire(t, word: bool):
         os.environ["RS_WORD_WIRE"] = "1"
     try:
         x0 = ctx.transfer_bytes()
-        A = rb.all_positions(t, mode="all", path="compact")
+        A = rb.all_positions(t, mode=mode, path="compact")
         x1 = ctx.transfer_bytes()
     finally:
         os.environ.pop("RS_WORD_WIRE", None)
@@ -751,9 +751,14 @@ def test_byte_wire_matches_word_wire(kind):
         assert d2h_bytes < 2 * n + T + (1 << 20), (d2h_bytes, n, T)
     if kind == "fibonacci":  # lengths far above 255: 32-bit wire
         assert int(A.lengths.max()) > 255 and d2h_bytes >= 4 * (2 * n + T)
+    L, d2h_lb = _all_with_wire(t, word=False, mode="leftmost")
+    LW, _ = _all_with_wire(t, word=True, mode="leftmost")
+    assert np.array_equal(L.starts, LW.starts) and np.array_equal(L.lengths, LW.lengths)
+    if kind == "iid":  # 2 bytes per position
+        assert d2h_lb < 2 * n + (1 << 20), (d2h_lb, n)
     from paper_1501_06663_b200.query import count_wrong_answers
     c = rb.build_compact_llr(rb.build_raw_llr(rb.build_suffix_structures(t)))
-    assert count_wrong_answers(c, n, all_answers=A) == 0
+    assert count_wrong_answers(c, n, all_answers=A, leftmost=L) == 0
 
 
 def test_byte_wire_shards():
@@ -791,3 +796,16 @@ def test_byte_wire_shards():
         base += f.size
     assert np.array_equal(lengths, full.lengths) and np.array_equal(offsets, full.offsets)
     assert np.array_equal(np.concatenate(flats), full.flat_starts)
+    left = rb.all_positions(rb.Text(data), mode="leftmost", path="compact")
+    for r in range(2):  # leftmost shards: (length, distance) byte pairs
+        lo, hi = D.shard_range(n, 2, r)
+        with ctx.lock:
+            tot = np.zeros(1, np.int64)
+            ctx.call("rs_query_structures_shard", 0, lo, hi, _native.i64(tot))
+            s_ = np.zeros(hi - lo, np.int64)
+            l_ = np.zeros(hi - lo, np.int64)
+            x0 = ctx.transfer_bytes()
+            ctx.call("rs_fetch_shard", 0, _native.i64(s_), _native.i64(l_), _native.i64(np.zeros(0, np.int64)))
+            x1 = ctx.transfer_bytes()
+        assert x1[1] - x0[1] < 2 * (hi - lo) + (1 << 20)
+        assert np.array_equal(s_, left.starts[lo:hi]) and np.array_equal(l_, left.lengths[lo:hi])
