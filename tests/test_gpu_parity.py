@@ -809,3 +809,31 @@ def test_byte_wire_shards():
             x1 = ctx.transfer_bytes()
         assert x1[1] - x0[1] < 2 * (hi - lo) + (1 << 20)
         assert np.array_equal(s_, left.starts[lo:hi]) and np.array_equal(l_, left.lengths[lo:hi])
+
+
+@pytest.mark.parametrize("kind", ["fibonacci", "periodic", "planted", "binary"])
+def test_text_order_round_keys_match_list_keys(kind):
+    """csrc/suffix_array.cu: doubling rounds with more than n/4 suffixes tied
+    build their keys in text order from the flagged ISA heads
+    (k_make_keys_text); RS_SA_LIST_KEYS=1 forces the slot-list gather.  Both
+    give the oracle's structures, and the repetitive inputs do take rounds of
+    each kind."""
+    data = {"fibonacci": lambda: workloads.fibonacci_mutated(300_000, 7, rate=1e-3),
+            "periodic": lambda: workloads.periodic_mutated(250_000, 3, period=977, rate=1e-3),
+            "planted": lambda: workloads.planted_dna(400_000, 5, family_len=400),
+            "binary": lambda: np.frombuffer(b"ab", np.uint8)[
+                np.random.default_rng(2).integers(0, 2, 200_000)]}[kind]()
+    want = oracle.build_suffix_structures(data, workers=8)
+    t = rb.Text(data)
+    prev = os.environ.pop("RS_SA_LIST_KEYS", None)
+    try:
+        for list_keys in (False, True):
+            if list_keys:
+                os.environ["RS_SA_LIST_KEYS"] = "1"
+            s = rb.build_suffix_structures(t)
+            os.environ.pop("RS_SA_LIST_KEYS", None)
+            assert np.array_equal(s.sa, want[0]), (kind, list_keys)
+            assert np.array_equal(s.rank, want[1]) and np.array_equal(s.lcp, want[2]), (kind, list_keys)
+    finally:
+        if prev is not None:
+            os.environ["RS_SA_LIST_KEYS"] = prev
