@@ -414,8 +414,10 @@ __global__ void __launch_bounds__(kUNT, sizeof(KeyT) == 4 ? 5 : 4) k_update(cons
             // next round's inputs: slot, group head (= new isa) and suffix,
             // so k_make_keys needs only the one random gather isa[i + h]
             P_next[o] = pos[j];
-            H_next[o] = (unsigned)run;
-            V_next[o] = v;
+            if (H_next) {  // null: the next round builds its keys in text order
+                H_next[o] = (unsigned)run;
+                V_next[o] = v;
+            }
             ++o;
         }
     }
@@ -1316,6 +1318,8 @@ void build_suffix_array(rs_ctx *c, long long n) {
     const bool key32 = bits * K <= 32;
     u64 *ks = nullptr;
     unsigned *ks32 = nullptr;
+    bool text_keys = false;  // the keys being consumed were built in text order
+    bool lists_ok = true;    // Ha / Va hold the head / suffix lists of the tied suffixes
     unsigned *vs;
     if (key32)
         radix_sort_pairs<unsigned>(c, (unsigned *)k0, (unsigned *)k1, v0, v1, n, bits * K, &ks32, &vs, &tk);
@@ -1368,9 +1372,13 @@ void build_suffix_array(rs_ctx *c, long long n) {
                         Va, tagg, tpre, lcp_d, bits, bits * K, be, sb_whole);
             tile_scan(tagg, tiles, tpre);
             if (!P) setup_round0_emit();
+            // head / suffix lists only when the next round may use the list
+            // gather (text-order rounds with more than n/2 tied skip them)
+            const bool lists = !P || !text_keys || 2 * U <= n;
             RS_LAUNCH_B(c, (P ? 24.0 : 28.0) * U, (k_update<false, u64>), (unsigned)tiles, kUNT, 0, ks, vs, P, U,
-                        P ? sa : (unsigned *)nullptr, isa, Pa, Ha, Va, tagg, tpre, P ? nullptr : lcp_d, bits,
-                        bits * K, be, sb_whole);
+                        P ? sa : (unsigned *)nullptr, isa, Pa, lists ? Ha : nullptr, lists ? Va : nullptr, tagg,
+                        tpre, P ? nullptr : lcp_d, bits, bits * K, be, sb_whole);
+            lists_ok = lists;
         }
         if (!P) {  // round 0: the sorted suffixes are the SA -- adopt their buffer instead of copying
             const BufId idv = (vs == (const unsigned *)c->bufs[B_VALS0].p) ? B_VALS0 : B_VALS1;
@@ -1449,7 +1457,8 @@ void build_suffix_array(rs_ctx *c, long long n) {
         // large rounds (most suffixes still tied): keys in text order, grouped
         // by head slot; smaller rounds: the list gather (dense ordinals when
         // they save radix passes)
-        const bool text_order = 4 * U > n && !std::getenv("RS_SA_LIST_KEYS");
+        const bool text_order = (4 * U > n || !lists_ok) && !std::getenv("RS_SA_LIST_KEYS");
+        text_keys = text_order;
         if (text_order) {
             unsigned long long *kc = (unsigned long long *)buf(c, B_SMALL, 4096) + 100;
             RS_CUDA(cudaMemsetAsync(kc, 0, sizeof(*kc), c->stream));
