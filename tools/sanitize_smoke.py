@@ -50,3 +50,23 @@ with ctx.lock:
         assert np.array_equal(a, A.lengths[lo:hi])
         assert np.array_equal(b - b[0], A.offsets[lo:hi + 1] - A.offsets[lo])
 print("sanitize smoke (round 2 paths) done")
+
+# byte wire (csrc/host_io.cu fetch_csr_bytes / fetch_leftmost_bytes): answers
+# of >= 4 Mi positions, all-ties and leftmost, full and shard fetches
+data = workloads.iid_dna((4 << 20) + 12345, 11)
+t = rb.Text(data)
+A = rb.all_positions(t, mode="all")
+L = rb.all_positions(t, mode="leftmost")
+n = t.n
+assert int(A.lengths.max()) <= 255 and A.offsets[-1] == A.flat_starts.size
+assert np.all(A.flat_starts[A.offsets[1:-1][np.diff(A.offsets[1:]) > 0]] >= 1)
+with ctx.lock:
+    ctx.call("rs_set_text", _native.u8(data), n)
+    ctx.call("rs_build_structures")
+    tot = np.zeros(1, np.int64)
+    ctx.call("rs_query_structures_shard", 0, 1, n + 1, _native.i64(tot))
+    s_ = np.empty(n, np.int64)
+    l_ = np.empty(n, np.int64)
+    ctx.call("rs_fetch_shard", 0, _native.i64(s_), _native.i64(l_), _native.i64(np.zeros(0, np.int64)))
+assert np.array_equal(s_, L.starts[1:]) and np.array_equal(l_, L.lengths[1:])
+print("sanitize smoke (byte wire) done")
