@@ -50,6 +50,8 @@ void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes);
 void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add);
 bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
                      long long L, long long T, long long *lengths, long long *offsets, long long *flat);
+bool fetch_csr_mixed(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
+                     long long L, long long T, long long *lengths, long long *offsets, long long *flat);
 bool fetch_leftmost_bytes(rs_ctx *c, const long long *d_starts, const long long *d_len, long long L, long long pos0,
                           long long *starts, long long *lengths);
 
@@ -765,6 +767,10 @@ int rs_fetch_all(rs_ctx *c, int64_t *lengths, int64_t *offsets, int64_t *flat) {
                             (const long long *)c->bufs[B_FLAT].p, n + 1, c->total, (long long *)lengths,
                             (long long *)offsets, (long long *)flat))
             return;
+        if (fetch_csr_mixed(c, (const long long *)c->bufs[B_OUT0].p, (const long long *)c->bufs[B_OUT1].p,
+                            (const long long *)c->bufs[B_FLAT].p, n + 1, c->total, (long long *)lengths,
+                            (long long *)offsets, (long long *)flat))
+            return;
         fetch_i64(c, (long long *)lengths, (const long long *)c->bufs[B_OUT0].p, n + 1, 0);
         fetch_i64(c, (long long *)offsets, (const long long *)c->bufs[B_OUT1].p, n + 2, 2);
         fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);
@@ -1072,6 +1078,9 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
         const long long *o0 = (const long long *)c->bufs[B_OUT0].p, *o1 = (const long long *)c->bufs[B_OUT1].p;
         if (mode == RS_MODE_ALL) {
             if (fetch_csr_bytes(c, o0, o1, (const long long *)c->bufs[B_FLAT].p, cnt, c->total, (long long *)a,
+                                (long long *)b, (long long *)flat))
+                return;
+            if (fetch_csr_mixed(c, o0, o1, (const long long *)c->bufs[B_FLAT].p, cnt, c->total, (long long *)a,
                                 (long long *)b, (long long *)flat))
                 return;
             fetch_i64(c, (long long *)a, o0, cnt, 0);

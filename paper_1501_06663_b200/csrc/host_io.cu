@@ -39,6 +39,7 @@ void widen_bytes(const unsigned char *w, long long *out, long long x, long long 
 void prefix_bytes(const unsigned char *w, long long *out, long long x, long long y, long long start, bool is_signed);
 void leftmost_pairs(const unsigned char *w, long long *starts, long long *lengths, long long x, long long y,
                     long long pos_x);
+void decode_block(const unsigned char *w, int width, int mode, long long *out, long long count, long long start);
 
 namespace {
 
@@ -424,6 +425,195 @@ bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, 
     if (T > 0)
         pipeline_bytes(c, d8, T, [&](const unsigned char *b, long long a, long long x, long long y) {
             prefix_bytes(b, flat + a, x, y, fs[(a + x) / kSample] - (long long)(signed char)b[x], true);
+        });
+    return true;
+}
+
+// ---- mixed-width wire: 1, 2 or 4 bytes per value, chosen per 2^16 block ----
+//
+// When some value does not fit a byte (long repeats: C5's lengths reach
+// 129453), the CSR still crosses PCIe as narrow as each block of kSample
+// values allows instead of falling back to 4 bytes everywhere: a block's
+// lengths, tie counts and start steps each take the width of that block's
+// largest value (steps signed).  Blocks are laid out back to back; the host
+// decodes each from its int64 sample.
+__device__ __forceinline__ unsigned char width_of(unsigned long long maxv) {
+    return maxv <= 0xffull ? 1 : (maxv <= 0xffffull ? 2 : 4);
+}
+__device__ __forceinline__ unsigned char swidth_of(long long lo, long long hi) {
+    return (lo >= -128 && hi <= 127) ? 1 : ((lo >= -32768 && hi <= 32767) ? 2 : 4);
+}
+__device__ __forceinline__ void put_w(unsigned char *p, int w, unsigned long long v) {
+    if (w == 1) *p = (unsigned char)v;
+    else if (w == 2) *reinterpret_cast<unsigned short *>(p) = (unsigned short)v;
+    else *reinterpret_cast<unsigned *>(p) = (unsigned)v;
+}
+
+// one CTA per block of positions: widths of its lengths and tie counts + sample
+__global__ void k_widths_pos(const long long *__restrict__ len, const long long *__restrict__ off, long long L,
+                             unsigned char *__restrict__ wl, unsigned char *__restrict__ wc,
+                             long long *__restrict__ osamp) {
+    const long long b = blockIdx.x, k0 = b * kSample, k1 = k0 + kSample < L ? k0 + kSample : L;
+    unsigned long long ml = 0, mc = 0;
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const unsigned long long l = (unsigned long long)len[k], cn = (unsigned long long)(off[k + 1] - off[k]);
+        ml = l > ml ? l : ml;
+        mc = cn > mc ? cn : mc;
+    }
+    __shared__ unsigned long long s_l[8], s_c[8];
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, ml, o), c2 = __shfl_xor_sync(0xffffffffu, mc, o);
+        ml = a > ml ? a : ml;
+        mc = c2 > mc ? c2 : mc;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_l[threadIdx.x >> 5] = ml;
+        s_c[threadIdx.x >> 5] = mc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            ml = s_l[i] > ml ? s_l[i] : ml;
+            mc = s_c[i] > mc ? s_c[i] : mc;
+        }
+        wl[b] = width_of(ml);
+        wc[b] = width_of(mc);
+        osamp[b] = off[k0];
+    }
+}
+
+// one CTA per block of ties: width of its start steps (the block's first step
+// is not sent: the block starts from its sample) + sample
+__global__ void k_widths_flat(const long long *__restrict__ flat, long long T, unsigned char *__restrict__ wf,
+                              long long *__restrict__ fsamp) {
+    const long long b = blockIdx.x, t0 = b * kSample, t1 = t0 + kSample < T ? t0 + kSample : T;
+    long long lo = 0, hi = 0;
+    for (long long t = t0 + 1 + threadIdx.x; t < t1; t += blockDim.x) {
+        const long long d = flat[t] - flat[t - 1];
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+    }
+    __shared__ long long s_lo[8], s_hi[8];
+    for (int o = 16; o; o >>= 1) {
+        const long long a = __shfl_xor_sync(0xffffffffu, lo, o), c2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = c2 > hi ? c2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            lo = s_lo[i] < lo ? s_lo[i] : lo;
+            hi = s_hi[i] > hi ? s_hi[i] : hi;
+        }
+        wf[b] = swidth_of(lo, hi);
+        fsamp[b] = flat[t0];
+    }
+}
+
+__global__ void k_pack_pos(const long long *__restrict__ len, const long long *__restrict__ off, long long L,
+                           const unsigned char *__restrict__ wl, const unsigned char *__restrict__ wc,
+                           const long long *__restrict__ lbase, const long long *__restrict__ cbase,
+                           unsigned char *__restrict__ lw, unsigned char *__restrict__ cw) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= L) return;
+    const long long b = k / kSample, i = k - b * kSample;
+    const int a = wl[b], c2 = wc[b];
+    put_w(lw + lbase[b] + i * a, a, (unsigned long long)len[k]);
+    put_w(cw + cbase[b] + i * c2, c2, (unsigned long long)(off[k + 1] - off[k]));
+}
+
+__global__ void k_pack_flat(const long long *__restrict__ flat, long long T, const unsigned char *__restrict__ wf,
+                            const long long *__restrict__ fbase, unsigned char *__restrict__ fw) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const long long b = t / kSample, i = t - b * kSample;
+    const int w = wf[b];
+    const long long d = i ? flat[t] - flat[t - 1] : 0;
+    put_w(fw + fbase[b] + i * w, w, (unsigned long long)d);
+}
+
+// D2H of a block-structured wire array (block b: bytes [base[b], base[b+1]),
+// `values` of them) through the pinned slots; decode(b, bytes) on the host threads.
+template <typename Decode>
+static void pipeline_blocks(rs_ctx *c, const unsigned char *dsrc, const std::vector<long long> &base, Decode decode) {
+    const long long nb = (long long)base.size() - 1, cap = 4 * kChunk;
+    std::vector<long long> cb{0};  // chunk boundaries (block indices)
+    for (long long b = 0; b < nb; ++b)
+        if (base[b + 1] - base[cb.back()] > cap) cb.push_back(b);
+    cb.push_back(nb);
+    const long long nch = (long long)cb.size() - 1;
+    Stage s = stage(c);
+    auto start = [&](long long i) {
+        const long long a = base[cb[i]], len = base[cb[i + 1]] - a;
+        RS_CUDA(cudaMemcpyAsync(s.host[i & 1], dsrc + a, (size_t)len, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h_bytes += len;
+        RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
+    };
+    start(0);
+    if (nch > 1) start(1);
+    Pool &pool = Pool::get();
+    for (long long i = 0; i < nch; ++i) {
+        RS_CUDA(cudaEventSynchronize(s.ev[i & 1]));
+        const unsigned char *w = (const unsigned char *)s.host[i & 1];
+        const long long b0 = cb[i], b1 = cb[i + 1], a = base[b0];
+        pool.run([&](int t, int T) {
+            long long x, y;
+            split(b1 - b0, t, T, x, y);
+            for (long long b = b0 + x; b < b0 + y; ++b) decode(b, w + (base[b] - a));
+        });
+        if (i + 2 < nch) start(i + 2);
+    }
+}
+
+bool fetch_csr_mixed(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
+                     long long L, long long T, long long *lengths, long long *offsets, long long *flat) {
+    if (L < (4ll << 20) || std::getenv("RS_WORD_WIRE")) return false;
+    const long long nb = (L + kSample - 1) / kSample, tb = (T + kSample - 1) / kSample;
+    // metadata: widths (3 arrays), samples, block byte bases (device copies)
+    const size_t meta = 16 * (size_t)(nb + tb + 2) + 8 * (size_t)(2 * (nb + 1) + tb + 1) + 256;
+    unsigned char *m = (unsigned char *)buf(c, B_XFER_ENDS, meta);
+    long long *osamp = (long long *)m, *fsamp = osamp + nb;
+    long long *lbase = fsamp + tb + 1, *cbase = lbase + nb + 1, *fbase = cbase + nb + 1;
+    unsigned char *wl = (unsigned char *)(fbase + tb + 1), *wc = wl + nb, *wf = wc + nb;
+    RS_LAUNCH(c, k_widths_pos, (unsigned)nb, 256, 0, d_len, d_off, L, wl, wc, osamp);
+    if (T > 0) RS_LAUNCH(c, k_widths_flat, (unsigned)tb, 256, 0, d_flat, T, wf, fsamp);
+    std::vector<unsigned char> w((size_t)(2 * nb + tb));
+    std::vector<long long> samp((size_t)(nb + tb));
+    d2h(c, w.data(), wl, w.size());
+    d2h(c, samp.data(), osamp, sizeof(long long) * samp.size());
+    RS_CUDA(cudaStreamSynchronize(c->stream));
+    const unsigned char *hwl = w.data(), *hwc = hwl + nb, *hwf = hwc + nb;
+    std::vector<long long> lb(nb + 1, 0), cbv(nb + 1, 0), fb(tb + 1, 0);
+    for (long long b = 0; b < nb; ++b) {
+        const long long cntb = std::min(kSample, L - b * kSample);
+        lb[b + 1] = lb[b] + cntb * hwl[b];
+        cbv[b + 1] = cbv[b] + cntb * hwc[b];
+    }
+    for (long long b = 0; b < tb; ++b) fb[b + 1] = fb[b] + std::min(kSample, T - b * kSample) * hwf[b];
+    h2d(c, lbase, lb.data(), sizeof(long long) * lb.size());
+    h2d(c, cbase, cbv.data(), sizeof(long long) * cbv.size());
+    if (T > 0) h2d(c, fbase, fb.data(), sizeof(long long) * fb.size());
+    auto r16 = [](long long v) { return (v + 15) & ~15ll; };  // 2- and 4-byte stores stay aligned
+    unsigned char *wire = (unsigned char *)buf(c, B_WIRE, (size_t)(r16(lb[nb]) + r16(cbv[nb]) + fb[tb]) + 64);
+    unsigned char *lw = wire, *cw = wire + r16(lb[nb]), *fw = cw + r16(cbv[nb]);
+    RS_LAUNCH_B(c, 24.0 * (double)L, k_pack_pos, grid_for(L, 256), 256, 0, d_len, d_off, L, wl, wc, lbase, cbase, lw,
+                cw);
+    if (T > 0) RS_LAUNCH_B(c, 16.0 * (double)T, k_pack_flat, grid_for(T, 256), 256, 0, d_flat, T, wf, fbase, fw);
+    const long long *os = samp.data(), *fs = samp.data() + nb;
+    pipeline_blocks(c, lw, lb, [&](long long b, const unsigned char *p) {
+        decode_block(p, hwl[b], 0, lengths + b * kSample, std::min(kSample, L - b * kSample), 0);
+    });
+    offsets[0] = os[0];
+    pipeline_blocks(c, cw, cbv, [&](long long b, const unsigned char *p) {
+        decode_block(p, hwc[b], 1, offsets + 1 + b * kSample, std::min(kSample, L - b * kSample), os[b]);
+    });
+    if (T > 0)
+        pipeline_blocks(c, fw, fb, [&](long long b, const unsigned char *p) {
+            decode_block(p, hwf[b], 2, flat + b * kSample, std::min(kSample, T - b * kSample), fs[b]);
         });
     return true;
 }

@@ -11,6 +11,7 @@
 #include <immintrin.h>
 
 #include <cstdint>
+#include <cstring>
 
 namespace rsb {
 
@@ -196,6 +197,39 @@ void leftmost_pairs(const unsigned char *w, long long *starts, long long *length
         const unsigned L = w[2 * j], d = w[2 * j + 1];
         lengths[j] = L;
         starts[j] = L ? pos_x + (j - x) - (long long)d : -1ll;
+    }
+}
+
+// One block of the mixed-width wire: `count` values of `width` bytes.
+// mode 0: out[j] = w[j]; mode 1: out[j] = start + w[0] + ... + w[j];
+// mode 2: the same with signed steps.
+template <typename U, typename S>
+static void decode_wide(const unsigned char *w, int mode, long long *out, long long count, long long start) {
+    const U *u = reinterpret_cast<const U *>(w);
+    long long run = start;
+    for (long long j = 0; j < count; ++j) {
+        U v;
+        std::memcpy(&v, u + j, sizeof(U));
+        long long x = mode == 2 ? (long long)(S)v : (long long)v;
+        if (mode == 0) {
+            _mm_stream_si64(reinterpret_cast<long long *>(out + j), x);
+        } else {
+            run += x;
+            _mm_stream_si64(reinterpret_cast<long long *>(out + j), run);
+        }
+    }
+    _mm_sfence();
+}
+
+void decode_block(const unsigned char *w, int width, int mode, long long *out, long long count, long long start) {
+    if (count <= 0) return;
+    if (width == 1) {
+        if (mode == 0) widen_bytes(w, out, 0, count);
+        else prefix_bytes(w, out, 0, count, start, mode == 2);
+    } else if (width == 2) {
+        decode_wide<unsigned short, short>(w, mode, out, count, start);
+    } else {
+        decode_wide<unsigned, int>(w, mode, out, count, start);
     }
 }
 

@@ -749,8 +749,8 @@ def test_byte_wire_matches_word_wire(kind):
     assert d2h_words >= 4 * (2 * n + T)  # 32-bit words (+ small readbacks)
     if kind == "iid":  # short repeats: the byte wire was used
         assert d2h_bytes < 2 * n + T + (1 << 20), (d2h_bytes, n, T)
-    if kind == "fibonacci":  # lengths far above 255: 32-bit wire
-        assert int(A.lengths.max()) > 255 and d2h_bytes >= 4 * (2 * n + T)
+    if kind == "fibonacci":  # lengths far above 255: the mixed-width wire (test_mixed_width_wire)
+        assert int(A.lengths.max()) > 255 and d2h_bytes < 4 * (2 * n + T)
     L, d2h_lb = _all_with_wire(t, word=False, mode="leftmost")
     LW, _ = _all_with_wire(t, word=True, mode="leftmost")
     assert np.array_equal(L.starts, LW.starts) and np.array_equal(L.lengths, LW.lengths)
@@ -837,3 +837,21 @@ def test_text_order_round_keys_match_list_keys(kind):
     finally:
         if prev is not None:
             os.environ["RS_SA_LIST_KEYS"] = prev
+
+
+def test_mixed_width_wire():
+    """csrc/host_io.cu fetch_csr_mixed: answers with values beyond a byte
+    (long repeats) cross PCIe 1, 2 or 4 bytes per value chosen per 2^16
+    block; identical to the 32-bit wire, and narrower than it."""
+    data = workloads.fibonacci_mutated(6_000_000, 9, rate=2e-4)
+    t = rb.Text(data)
+    A, d2h_mixed = _all_with_wire(t, word=False)
+    W, d2h_words = _all_with_wire(t, word=True)
+    assert int(A.lengths.max()) > 255  # the byte wire cannot carry it
+    assert np.array_equal(A.lengths, W.lengths) and np.array_equal(A.offsets, W.offsets)
+    assert np.array_equal(A.flat_starts, W.flat_starts)
+    n, T = data.size, A.flat_starts.size
+    assert d2h_mixed < 0.6 * d2h_words, (d2h_mixed, d2h_words)
+    from paper_1501_06663_b200.query import count_wrong_answers
+    c = rb.build_compact_llr(rb.build_raw_llr(rb.build_suffix_structures(t)))
+    assert count_wrong_answers(c, n, all_answers=A) == 0
