@@ -394,14 +394,11 @@ __global__ void __launch_bounds__(kNT) k_query(const uint2 *__restrict__ e, cons
     __shared__ unsigned s_warp[kNT / 32];
     __shared__ u64 s_base;
 
-    long long tile;
-    if (ALL) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
-        __syncthreads();
-        tile = s_tile;
-    } else {
-        tile = blockIdx.x;
-    }
+    // tile = blockIdx.x also for the look-back of the all variant (dispatch
+    // order, as k_query_fused; see lookback_warp)
+    (void)counter;
+    (void)s_tile;
+    const long long tile = blockIdx.x;
     TileCtx<unsigned> x;
     x.tile = tile;
     const long long lo = bounds[2 * tile], hi = bounds[2 * tile + 1];
