@@ -52,6 +52,8 @@ bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, 
                      long long L, long long T, long long *lengths, long long *offsets, long long *flat);
 bool fetch_csr_mixed(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
                      long long L, long long T, long long *lengths, long long *offsets, long long *flat);
+bool fetch_leftmost_mixed(rs_ctx *c, const long long *d_starts, const long long *d_len, long long L, long long pos0,
+                          long long *starts, long long *lengths);
 bool fetch_leftmost_bytes(rs_ctx *c, const long long *d_starts, const long long *d_len, long long L, long long pos0,
                           long long *starts, long long *lengths);
 
@@ -754,6 +756,9 @@ int rs_fetch_leftmost(rs_ctx *c, int64_t *starts, int64_t *lengths) {
         if (fetch_leftmost_bytes(c, (const long long *)c->bufs[B_OUT0].p, (const long long *)c->bufs[B_OUT1].p,
                                  n + 1, 0, (long long *)starts, (long long *)lengths))
             return;
+        if (fetch_leftmost_mixed(c, (const long long *)c->bufs[B_OUT0].p, (const long long *)c->bufs[B_OUT1].p,
+                                 n + 1, 0, (long long *)starts, (long long *)lengths))
+            return;
         fetch_i64(c, (long long *)starts, (const long long *)c->bufs[B_OUT0].p, n + 1, 1);
         fetch_i64(c, (long long *)lengths, (const long long *)c->bufs[B_OUT1].p, n + 1, 0);
     });
@@ -1088,6 +1093,7 @@ int rs_fetch_shard(rs_ctx *c, int mode, int64_t *a, int64_t *b, int64_t *flat) {
             fetch_i64(c, (long long *)flat, (const long long *)c->bufs[B_FLAT].p, c->total, 0);
         } else {
             if (fetch_leftmost_bytes(c, o0, o1, cnt, c->shard_lo, (long long *)a, (long long *)b)) return;
+            if (fetch_leftmost_mixed(c, o0, o1, cnt, c->shard_lo, (long long *)a, (long long *)b)) return;
             fetch_i64(c, (long long *)a, o0, cnt, 1);
             fetch_i64(c, (long long *)b, o1, cnt, 0);
         }

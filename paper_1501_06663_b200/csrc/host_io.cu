@@ -40,6 +40,8 @@ void prefix_bytes(const unsigned char *w, long long *out, long long x, long long
 void leftmost_pairs(const unsigned char *w, long long *starts, long long *lengths, long long x, long long y,
                     long long pos_x);
 void decode_block(const unsigned char *w, int width, int mode, long long *out, long long count, long long start);
+void decode_left_block(const unsigned char *w, int width, long long count, long long pos0, long long *starts,
+                       long long *lengths);
 
 namespace {
 
@@ -615,6 +617,64 @@ bool fetch_csr_mixed(rs_ctx *c, const long long *d_len, const long long *d_off, 
         pipeline_blocks(c, fw, fb, [&](long long b, const unsigned char *p) {
             decode_block(p, hwf[b], 2, flat + b * kSample, std::min(kSample, T - b * kSample), fs[b]);
         });
+    return true;
+}
+
+// Leftmost answers over the mixed-width wire: per block of 2^16 slots one
+// width (that of the block's longest answer; position - start is smaller),
+// the block's lengths then its position - start values.
+__global__ void k_widths_left(const long long *__restrict__ len, long long L, unsigned char *__restrict__ wl) {
+    const long long b = blockIdx.x, k0 = b * kSample, k1 = k0 + kSample < L ? k0 + kSample : L;
+    unsigned long long ml = 0;
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const unsigned long long l = (unsigned long long)len[k];
+        ml = l > ml ? l : ml;
+    }
+    __shared__ unsigned long long s_l[8];
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, ml, o);
+        ml = a > ml ? a : ml;
+    }
+    if ((threadIdx.x & 31) == 0) s_l[threadIdx.x >> 5] = ml;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) ml = s_l[i] > ml ? s_l[i] : ml;
+        wl[b] = width_of(ml);
+    }
+}
+
+__global__ void k_pack_left(const long long *__restrict__ starts, const long long *__restrict__ len, long long L,
+                            long long pos0, const unsigned char *__restrict__ wl,
+                            const long long *__restrict__ base, unsigned char *__restrict__ wire) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= L) return;
+    const long long b = k / kSample, i = k - b * kSample, cntb = (L - b * kSample) < kSample ? L - b * kSample : kSample;
+    const int w = wl[b];
+    const long long l = len[k];
+    put_w(wire + base[b] + i * w, w, (unsigned long long)l);
+    put_w(wire + base[b] + (cntb + i) * w, w, (unsigned long long)(l ? pos0 + k - starts[k] : 0));
+}
+
+bool fetch_leftmost_mixed(rs_ctx *c, const long long *d_starts, const long long *d_len, long long L, long long pos0,
+                          long long *starts, long long *lengths) {
+    if (L < (4ll << 20) || std::getenv("RS_WORD_WIRE")) return false;
+    const long long nb = (L + kSample - 1) / kSample;
+    unsigned char *m = (unsigned char *)buf(c, B_XFER_ENDS, 8 * (size_t)(nb + 1) + (size_t)nb + 64);
+    long long *base = (long long *)m;
+    unsigned char *wl = (unsigned char *)(base + nb + 1);
+    RS_LAUNCH(c, k_widths_left, (unsigned)nb, 256, 0, d_len, L, wl);
+    std::vector<unsigned char> w((size_t)nb);
+    d2h(c, w.data(), wl, w.size());
+    RS_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<long long> bs(nb + 1, 0);
+    for (long long b = 0; b < nb; ++b) bs[b + 1] = bs[b] + 2 * std::min(kSample, L - b * kSample) * w[b];
+    h2d(c, base, bs.data(), sizeof(long long) * bs.size());
+    unsigned char *wire = (unsigned char *)buf(c, B_WIRE, (size_t)bs[nb] + 64);
+    RS_LAUNCH_B(c, 16.0 * (double)L, k_pack_left, grid_for(L, 256), 256, 0, d_starts, d_len, L, pos0, wl, base, wire);
+    pipeline_blocks(c, wire, bs, [&](long long b, const unsigned char *p) {
+        decode_left_block(p, w[b], std::min(kSample, L - b * kSample), pos0 + b * kSample, starts + b * kSample,
+                          lengths + b * kSample);
+    });
     return true;
 }
 

@@ -233,4 +233,28 @@ void decode_block(const unsigned char *w, int width, int mode, long long *out, l
     }
 }
 
+// One leftmost block of the mixed-width wire: `count` lengths then `count`
+// position - start values, `width` bytes each; slot j answers position pos0 + j.
+template <typename U>
+static void decode_left_wide(const unsigned char *w, long long count, long long pos0, long long *starts,
+                             long long *lengths) {
+    const U *l = reinterpret_cast<const U *>(w), *d = l + count;
+    for (long long j = 0; j < count; ++j) {
+        U lv, dv;
+        std::memcpy(&lv, l + j, sizeof(U));
+        std::memcpy(&dv, d + j, sizeof(U));
+        _mm_stream_si64(reinterpret_cast<long long *>(lengths + j), (long long)lv);
+        _mm_stream_si64(reinterpret_cast<long long *>(starts + j), lv ? pos0 + j - (long long)dv : -1ll);
+    }
+    _mm_sfence();
+}
+
+void decode_left_block(const unsigned char *w, int width, long long count, long long pos0, long long *starts,
+                       long long *lengths) {
+    if (count <= 0) return;
+    if (width == 1) decode_left_wide<unsigned char>(w, count, pos0, starts, lengths);
+    else if (width == 2) decode_left_wide<unsigned short>(w, count, pos0, starts, lengths);
+    else decode_left_wide<unsigned>(w, count, pos0, starts, lengths);
+}
+
 }  // namespace rsb

@@ -852,6 +852,47 @@ def test_mixed_width_wire():
     assert np.array_equal(A.flat_starts, W.flat_starts)
     n, T = data.size, A.flat_starts.size
     assert d2h_mixed < 0.6 * d2h_words, (d2h_mixed, d2h_words)
+    L, d2h_lm = _all_with_wire(t, word=False, mode="leftmost")  # (length, position - start) per block width
+    LW, d2h_lw = _all_with_wire(t, word=True, mode="leftmost")
+    assert np.array_equal(L.starts, LW.starts) and np.array_equal(L.lengths, LW.lengths)
+    assert d2h_lm < 0.6 * d2h_lw, (d2h_lm, d2h_lw)
     from paper_1501_06663_b200.query import count_wrong_answers
     c = rb.build_compact_llr(rb.build_raw_llr(rb.build_suffix_structures(t)))
-    assert count_wrong_answers(c, n, all_answers=A) == 0
+    assert count_wrong_answers(c, n, all_answers=A, leftmost=L) == 0
+
+
+def test_mixed_width_wire_shards():
+    """rs_fetch_shard over the mixed-width wire (long repeats, shards of
+    >= 4 Mi positions): stitched shards == the full answers."""
+    from paper_1501_06663_b200 import _native
+    from paper_1501_06663_b200 import distributed as D
+    data = workloads.fibonacci_mutated(9_000_000, 13, rate=2e-4)
+    n = data.size
+    t = rb.Text(data)
+    full = rb.all_positions(t, mode="all", path="compact")
+    left = rb.all_positions(t, mode="leftmost", path="compact")
+    assert int(full.lengths.max()) > 255
+    ctx = _native.context()
+    with ctx.lock:
+        ctx.call("rs_set_text", _native.u8(data), n)
+        ctx.call("rs_build_structures")
+    flats, base = [], 0
+    for r in range(2):
+        lo, hi = D.shard_range(n, 2, r)
+        with ctx.lock:
+            tot = np.zeros(1, np.int64)
+            ctx.call("rs_query_structures_shard", 1, lo, hi, _native.i64(tot))
+            ctx.call("rs_shard_rebase", base)
+            a = np.zeros(hi - lo, np.int64)
+            b = np.zeros(hi - lo + 1, np.int64)
+            f = np.zeros(int(tot[0]), np.int64)
+            ctx.call("rs_fetch_shard", 1, _native.i64(a), _native.i64(b), _native.i64(f))
+            ctx.call("rs_query_structures_shard", 0, lo, hi, _native.i64(tot))
+            s_ = np.zeros(hi - lo, np.int64)
+            l_ = np.zeros(hi - lo, np.int64)
+            ctx.call("rs_fetch_shard", 0, _native.i64(s_), _native.i64(l_), _native.i64(np.zeros(0, np.int64)))
+        assert np.array_equal(a, full.lengths[lo:hi]) and np.array_equal(b, full.offsets[lo:hi + 1])
+        assert np.array_equal(s_, left.starts[lo:hi]) and np.array_equal(l_, left.lengths[lo:hi])
+        flats.append(f)
+        base += f.size
+    assert np.array_equal(np.concatenate(flats), full.flat_starts)
