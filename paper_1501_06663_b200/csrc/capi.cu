@@ -45,7 +45,7 @@ bool query_range(rs_ctx *c, int mode, int path, const uint2 *d_e, long long coun
 
 void fetch_i64(rs_ctx *c, long long *dst, const long long *dsrc, long long count, int kind);
 bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long count, long long lo, long long hi,
-                    long long add);
+                    long long add, bool bytes = false);
 void put_bytes(rs_ctx *c, void *ddst, const void *src, size_t bytes);
 void fetch_u32_as_i64(rs_ctx *c, long long *dst, const unsigned *dsrc, long long count, long long add);
 bool fetch_csr_bytes(rs_ctx *c, const long long *d_len, const long long *d_off, const long long *d_flat,
@@ -583,7 +583,7 @@ int rs_set_structures(rs_ctx *c, const int64_t *sa, const int64_t *rank, const i
             }
             if (!put_i64_as_u32(c, disa, (const long long *)rank + 1, n, 1, n, -1))
                 fail(RS_EINVAL, "rank has values out of range");
-            if (!put_i64_as_u32(c, dlcp, (const long long *)lcp + 1, n + 1, 0, n, 0))
+            if (!put_i64_as_u32(c, dlcp, (const long long *)lcp + 1, n + 1, 0, n, 0, true))
                 fail(RS_EINVAL, "lcp has values out of range");
         }
         // The reference computes raw LLR from rank and lcp (_kernels_numba.py:33-38).

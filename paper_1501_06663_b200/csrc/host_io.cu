@@ -40,6 +40,9 @@ void prefix_bytes(const unsigned char *w, long long *out, long long x, long long
 void leftmost_pairs(const unsigned char *w, long long *starts, long long *lengths, long long x, long long y,
                     long long pos_x);
 void decode_block(const unsigned char *w, int width, int mode, long long *out, long long count, long long start);
+bool narrow_words(const long long *in, unsigned *w, long long x, long long y, long long lo, long long hi,
+                  long long add);
+int narrow_bytes(const long long *in, unsigned char *b, long long x, long long y, long long lo, long long hi);
 void decode_left_block(const unsigned char *w, int width, long long count, long long pos0, long long *starts,
                        long long *lengths);
 
@@ -703,35 +706,72 @@ bool fetch_leftmost_bytes(rs_ctx *c, const long long *d_starts, const long long 
 // H2D of `count` int64 values into a device u32 array, each checked to lie in
 // [lo, hi] and stored as value + add.  Returns false (nothing usable written)
 // if a value is out of range.
+__global__ void k_expand_bytes(const unsigned char *__restrict__ b, unsigned *__restrict__ out, long long count,
+                               unsigned add) {
+    const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < count) {
+        const uchar4 v = *reinterpret_cast<const uchar4 *>(b + i);
+        out[i] = v.x + add;
+        out[i + 1] = v.y + add;
+        out[i + 2] = v.z + add;
+        out[i + 3] = v.w + add;
+    } else {
+        for (long long j = i; j < count; ++j) out[j] = b[j] + add;
+    }
+}
+
+// bytes: values of at most 255 (LCP of short-repeat texts) cross PCIe as one
+// byte each and are widened on the device, chunk by chunk (a chunk with a
+// larger value goes as 32-bit words)
 bool put_i64_as_u32(rs_ctx *c, unsigned *ddst, const long long *src, long long count, long long lo, long long hi,
-                    long long add) {
+                    long long add, bool bytes) {
     if (count <= 0) return true;
     Stage s = stage(c);
     Pool &pool = Pool::get();
     const long long nch = (count + kChunk - 1) / kChunk;
-    std::atomic<bool> bad{false};
+    unsigned char *ring = bytes ? (unsigned char *)buf(c, B_XFER, 2 * 4 * (size_t)kChunk) : nullptr;
+    std::atomic<int> bad{0};
     for (long long i = 0; i < nch; ++i) {
         const long long a = i * kChunk, len = std::min(kChunk, count - a);
         if (i >= 2) RS_CUDA(cudaEventSynchronize(s.ev[i & 1]));  // slot free again
-        unsigned *w = (unsigned *)s.host[i & 1];
         const long long *in = src + a;
-        pool.run([&](int t, int T) {
-            long long x, y;
-            split(len, t, T, x, y);
-            bool ok = true;
-            for (long long j = x; j < y; ++j) {
-                const long long v = in[j];
-                ok &= (v >= lo) & (v <= hi);
-                w[j] = (unsigned)(v + add);
+        bool as_bytes = false;
+        if (bytes) {
+            unsigned char *b = (unsigned char *)s.host[i & 1];
+            bad.store(0);
+            pool.run([&](int t, int T) {
+                long long x, y;
+                split(len, t, T, x, y);
+                const int r = narrow_bytes(in, b, x, y, lo, hi);
+                if (r) bad.fetch_or(r, std::memory_order_relaxed);
+            });
+            if (bad.load() & 1) {
+                RS_CUDA(cudaStreamSynchronize(c->stream));
+                return false;
             }
-            if (!ok) bad.store(true, std::memory_order_relaxed);
-        });
-        if (bad.load()) {
-            RS_CUDA(cudaStreamSynchronize(c->stream));
-            return false;
+            as_bytes = bad.load() == 0;
+            if (as_bytes) {
+                unsigned char *d = ring + (size_t)(i & 1) * 4 * kChunk;
+                RS_CUDA(cudaMemcpyAsync(d, b, (size_t)len, cudaMemcpyHostToDevice, c->stream));
+                c->h2d_bytes += len;
+                RS_LAUNCH(c, k_expand_bytes, grid_for((len + 3) / 4, 256), 256, 0, d, ddst + a, len, (unsigned)add);
+            }
         }
-        RS_CUDA(cudaMemcpyAsync(ddst + a, w, 4 * (size_t)len, cudaMemcpyHostToDevice, c->stream));
-        c->h2d_bytes += 4 * len;
+        if (!as_bytes) {
+            unsigned *w = (unsigned *)s.host[i & 1];
+            bad.store(0);
+            pool.run([&](int t, int T) {
+                long long x, y;
+                split(len, t, T, x, y);
+                if (!narrow_words(in, w, x, y, lo, hi, add)) bad.store(1, std::memory_order_relaxed);
+            });
+            if (bad.load()) {
+                RS_CUDA(cudaStreamSynchronize(c->stream));
+                return false;
+            }
+            RS_CUDA(cudaMemcpyAsync(ddst + a, w, 4 * (size_t)len, cudaMemcpyHostToDevice, c->stream));
+            c->h2d_bytes += 4 * len;
+        }
         RS_CUDA(cudaEventRecord(s.ev[i & 1], c->stream));
     }
     RS_CUDA(cudaStreamSynchronize(c->stream));

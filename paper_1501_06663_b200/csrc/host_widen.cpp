@@ -257,4 +257,69 @@ void decode_left_block(const unsigned char *w, int width, long long count, long 
     else decode_left_wide<unsigned>(w, count, pos0, starts, lengths);
 }
 
+// ---- H2D narrowing (host_io.cu put_i64_as_u32) ------------------------------
+
+// w[j] = in[j] + add for j in [x, y); false if some in[j] lies outside [lo, hi]
+__attribute__((target("avx2"))) static bool narrow_avx2(const long long *in, unsigned *w, long long x, long long y,
+                                                        long long lo, long long hi, long long add) {
+    long long j = x;
+    bool ok = true;
+    while (j < y && (reinterpret_cast<uintptr_t>(w + j) & 31)) {
+        const long long v = in[j];
+        ok &= (v >= lo) & (v <= hi);
+        w[j] = (unsigned)(v + add);
+        ++j;
+    }
+    const __m256i vlo = _mm256_set1_epi64x(lo), vhi = _mm256_set1_epi64x(hi), vadd = _mm256_set1_epi64x(add);
+    const __m256i pick = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+    __m256i badv = _mm256_setzero_si256();
+    for (; j + 8 <= y; j += 8) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(in + j));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(in + j + 4));
+        // lo > v or v > hi: out of range
+        badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(vlo, a), _mm256_cmpgt_epi64(a, vhi)));
+        badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(vlo, b), _mm256_cmpgt_epi64(b, vhi)));
+        const __m256i pa = _mm256_permutevar8x32_epi32(_mm256_add_epi64(a, vadd), pick);  // low words in lanes 0-3
+        const __m256i pb = _mm256_permutevar8x32_epi32(_mm256_add_epi64(b, vadd), pick);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(w + j), _mm256_permute2x128_si256(pa, pb, 0x20));
+    }
+    ok &= _mm256_testz_si256(badv, badv) != 0;
+    for (; j < y; ++j) {
+        const long long v = in[j];
+        ok &= (v >= lo) & (v <= hi);
+        w[j] = (unsigned)(v + add);
+    }
+    _mm_sfence();
+    return ok;
+}
+
+bool narrow_words(const long long *in, unsigned *w, long long x, long long y, long long lo, long long hi,
+                  long long add) {
+    if (y <= x) return true;
+    if (have_avx2()) return narrow_avx2(in, w, x, y, lo, hi, add);
+    bool ok = true;
+    for (long long j = x; j < y; ++j) {
+        const long long v = in[j];
+        ok &= (v >= lo) & (v <= hi);
+        w[j] = (unsigned)(v + add);
+    }
+    return ok;
+}
+
+// b[j] = in[j] for j in [x, y) when every value lies in [0, 255]; returns
+// 0 if so, 1 if some value is outside [lo, hi] (an error), 2 if all are in
+// [lo, hi] but some exceeds a byte (send 32-bit words instead)
+int narrow_bytes(const long long *in, unsigned char *b, long long x, long long y, long long lo, long long hi) {
+    unsigned long long big = 0;
+    bool ok = true;
+    for (long long j = x; j < y; ++j) {
+        const long long v = in[j];
+        ok &= (v >= lo) & (v <= hi);
+        big |= (unsigned long long)v;
+        b[j] = (unsigned char)v;
+    }
+    if (!ok) return 1;
+    return big > 255ull ? 2 : 0;
+}
+
 }  // namespace rsb
