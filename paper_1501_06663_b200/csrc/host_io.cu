@@ -140,7 +140,10 @@ inline void split(long long count, int t, int T, long long &a, long long &b) {
     b = std::min(count, a + per);
 }
 
-constexpr long long kChunk = 16ll << 20;        // values per pipeline slot (64 MiB on the wire)
+#ifndef RS_XFER_CHUNK
+#define RS_XFER_CHUNK (16ll << 20)
+#endif
+constexpr long long kChunk = RS_XFER_CHUNK;     // values per pipeline slot (64 MiB of 32-bit words)
 constexpr size_t kMinStaged = 8u << 20;         // smaller arrays: one plain copy
 
 __global__ void k_narrow_words(const long long *__restrict__ src, unsigned *__restrict__ dst, long long count) {
