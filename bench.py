@@ -427,7 +427,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_1501_06663_b200 import distributed
-        distributed.bench_main(args)
+        distributed.bench_main(args, tools={"ClockSampler": ClockSampler, "roofline_of": roofline_of})
         return
     run_single(args)
 

@@ -495,7 +495,7 @@ def to_answers(out, mode: str):
 # ---------------------------------------------------------------------------------------
 # bench (torchrun, N > 1)
 # ---------------------------------------------------------------------------------------
-def bench_main(args) -> None:
+def bench_main(args, tools: dict | None = None) -> None:
     """torchrun bench (N > 1): the same metric and config as bench.py at N = 1,
     strong scaling over one text.
 
@@ -548,6 +548,9 @@ def bench_main(args) -> None:
         def step():
             return structures_query_shard(ctx, n, "all", None, device)
 
+        clocks = tools["ClockSampler"](local) if tools else None
+        if clocks:
+            clocks.start()  # spans warm-up, timed and instrumented steps
         for _ in range(args.warmup):
             step()
         dist.barrier()
@@ -562,6 +565,13 @@ def bench_main(args) -> None:
         ms = ctx.elapsed_ms(0, 1) / args.steps
         launches = ctx.launches() - l0
         stages = ctx.stage_times()
+        # per-kernel breakdown of this rank's shard step (separate instrumented pass)
+        ctx.profile_begin()
+        for _ in range(args.steps):
+            step()
+        ctx.synchronize()
+        profile = ctx.profile_end()
+        clk = clocks.stop() if clocks else None
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -587,6 +597,22 @@ def bench_main(args) -> None:
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         if i >= args.warmup:
             e2e.append(float(dt.item()))
+    # clocks of every rank's GPU: slowest median, union of throttle reasons
+    clks = [None] * world
+    dist.all_gather_object(clks, clk)
+    clks = [c for c in clks if c]
+    clocks_line = None
+    if clks:
+        meds = [c["sm_mhz"] for c in clks if c.get("sm_mhz") is not None]
+        maxs = [c["sm_max_mhz"] for c in clks if c.get("sm_max_mhz") is not None]
+        clocks_line = {"sm_mhz": min(meds) if meds else None, "sm_max_mhz": max(maxs) if maxs else None,
+                       "reasons": sorted({r for c in clks for r in c.get("reasons", [])}),
+                       "ranks": len(clks)}
+    roof = None
+    if tools and profile:
+        roof, _ = tools["roofline_of"](profile, args.steps)
+        roof["traffic"] = None  # the committed ncu capture is of the full-size (N = 1) launch
+        roof["traffic_source"] = "rank 0's shard launch (1/N of the positions): not captured"
     # bytes the library copied host<->device in the timed calls, summed over ranks
     xfer = torch.tensor([b - a for a, b in zip(xfer0, ctx.transfer_bytes())], dtype=torch.float64, device=device)
     dist.all_reduce(xfer, op=dist.ReduceOp.SUM)
@@ -606,6 +632,8 @@ def bench_main(args) -> None:
                        "l2": "input 256 MiB > 126 MB L2; raw LLR, compaction and answers rebuilt each step",
                        "T": T},
             "gpu_launches": int(round(float(lt.item()))),
+            "clocks": clocks_line,
+            "roofline": roof,
             "stages_ms_rank0": stages,
             "e2e": {"value": n / float(np.mean(e2e)), "unit": "positions/s", "h2d_bytes_per_step": h2d_step,
                     "d2h_bytes_per_step": d2h_step, "answer_bytes_per_step": 8 * (n + 1) + 8 * (n + 2) + 8 * T,
