@@ -78,7 +78,30 @@ __global__ void k_bounds(const uint2 *__restrict__ e, const unsigned *__restrict
     if (RAW) {
         // search in [min_lo, kfirst]; answer kfirst+1 if none (min_lo > 1: a
         // shard's raw array starts there -- it is below every covering start)
-        long long a = min_lo > 1 ? min_lo : 1, b = kfirst + 1;
+        // i + raw[i] - 1 >= kfirst is monotone in i; gallop left from kfirst
+        // (the answer lies within the longest repeat length of it) before
+        // bisecting: ~2 log2(LLR) probes instead of log2(n)
+        const long long a0 = min_lo > 1 ? min_lo : 1;
+        long long a = a0, b = kfirst + 1;
+        if (kfirst < a0) {
+            // (empty search range: as the plain bisection, lo = a0)
+        } else if (kfirst + (long long)__ldg(raw + kfirst) - 1 >= kfirst) {
+            b = kfirst;
+            long long step = 1;
+            while (true) {
+                const long long probe = kfirst - step;
+                if (probe < a0) { a = a0; break; }
+                if (probe + (long long)__ldg(raw + probe) - 1 >= kfirst) {
+                    b = probe;
+                    step <<= 1;
+                } else {
+                    a = probe + 1;
+                    break;
+                }
+            }
+        } else {
+            a = b;  // nothing at or before kfirst reaches it
+        }
         while (a < b) {
             long long mid = (a + b) >> 1;
             if (mid + (long long)__ldg(raw + mid) - 1 >= kfirst) b = mid; else a = mid + 1;
